@@ -1,0 +1,185 @@
+/*
+ * ndf_b200.h -- C-ABI of the B200-native NDF hot path (libndf_b200.so).
+ *
+ * Plain pointers and sizes only: every device pointer is borrowed (the
+ * caller -- PyTorch on the Python side -- owns the memory), every call takes
+ * a CUDA stream handle (`void*` = cudaStream_t), is stream-ordered and
+ * asynchronous, and returns an ndf_status (0 = OK).  On failure
+ * ndf_last_error() returns a thread-local message.
+ *
+ * The reference (/root/reference/pkg/src/ndf) is pure Python; its "FFI"
+ * for this path is the Python call surface each entry point replaces,
+ * cited per function below.  INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef NDF_B200_H
+#define NDF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NDF_ABI_VERSION 1
+#define NDF_MAX_LAYERS 8
+#define NDF_MAX_WIDTH 256
+
+/* status codes; mapped onto the reference's NdfError tree (errors.py:4-49) */
+typedef enum {
+  NDF_OK = 0,
+  NDF_ERR_PARAMETER = 1,   /* ParameterError   (errors.py:24) */
+  NDF_ERR_SHAPE = 2,       /* ShapeError       (errors.py:36) */
+  NDF_ERR_CONFIG = 3,      /* ConfigError      (errors.py:40) */
+  NDF_ERR_CUDA = 4,        /* DeviceError (new: CUDA runtime failure) */
+  NDF_ERR_UNSUPPORTED = 5, /* ConfigError: shape outside the kernels' envelope */
+  NDF_ERR_DEGENERATE = 6   /* ParameterError raised by digamma(0), measures.py:143-144 */
+} ndf_status;
+
+/* merge modes: model.py:26 plus BASELINE's [a+b, |a-b|] */
+enum { NDF_MERGE_MULTIPLY = 0, NDF_MERGE_CONCAT = 1, NDF_MERGE_ADD = 2,
+       NDF_MERGE_ABSDIFF = 3, NDF_MERGE_SUM_ABSDIFF = 4 };
+/* hidden activations: nn.py:23-32 plus SiLU */
+enum { NDF_ACT_RELU = 0, NDF_ACT_SNAKE = 1, NDF_ACT_SNAKE_ALT = 2, NDF_ACT_SILU = 3 };
+/* output head: linear (reference, nn.py:136), tanh (Pearson), softplus (MI) */
+enum { NDF_HEAD_LINEAR = 0, NDF_HEAD_TANH = 1, NDF_HEAD_SOFTPLUS = 2 };
+/* query precision */
+enum { NDF_PREC_FP32 = 0,   /* SIMT fp32, sequential k-sum (nn.py:18-20 order) */
+       NDF_PREC_BF16 = 1 }; /* tcgen05 bf16 x bf16 -> fp32 TMEM accumulators */
+
+/*
+ * Model descriptor (host struct, device pointers inside).
+ * Mirrors ModelSpec/NdfModel (model.py:29-142) for encoder_layers == 0 with
+ * one dense latent level per branch (the BASELINE architecture).
+ */
+typedef struct ndf_model_desc {
+  int32_t fourier_octaves;        /* L: 6L Fourier features (encoding.py:22-51) */
+  int32_t grid_channels;          /* C: latent channels (features_per_level) */
+  int32_t grid_res[3];            /* latent resolution along x, y, z */
+  int32_t merge;                  /* NDF_MERGE_* */
+  int32_t activation;             /* NDF_ACT_* (hidden layers) */
+  int32_t head;                   /* NDF_HEAD_* */
+  int32_t n_layers;               /* decoder affine layers incl. output layer */
+  int32_t widths[NDF_MAX_LAYERS + 1]; /* decoder widths [in, h1, ..., 1] */
+  const float* grid_mu;           /* device (rz, ry, rx, C) fp32 */
+  const float* grid_nu;           /* device; == grid_mu for shared models */
+  const float* params_f32;        /* device: W0 (in x h1, row-major), b0, W1, b1, ...
+                                     -- the NDFM/parameters() order (model.py:148-157) */
+  const void* params_tc;          /* device: ndf_tc_pack() output, or NULL */
+} ndf_model_desc;
+
+int32_t ndf_abi_version(void);
+const char* ndf_last_error(void);
+/* number of SMs of the current device (grid sizing), or -1 */
+int32_t ndf_device_sm_count(void);
+
+/* ---- NDF query ------------------------------------------------------------ */
+
+/* Bytes of the packed tensor-core parameter blob for this model (0 if the
+ * model is outside the tcgen05 kernel's envelope: hidden width 128, input
+ * width <= 128, >= 2 affine layers, output width 1). */
+size_t ndf_tc_blob_bytes(const ndf_model_desc* m);
+/* Pack params_f32 into the UMMA-canonical bf16 blob (device kernel).
+ * Replaces nothing in the reference: it is the "validate once at upload"
+ * step (failure detection). */
+int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_bytes, void* stream);
+
+/* Reference-to-all-vertices query over an output grid (x fastest).
+ * Replaces service.reconstruct_field (service.py:46-84): the ref point is
+ * embedded once, every query vertex once; writes out[v - v0] for flat
+ * vertices v in [v0, v1).  ref_is_mu selects ROLE_MU / ROLE_NU
+ * (service.py:63-80). */
+int ndf_query_grid(const ndf_model_desc* m, double ref_x, double ref_y, double ref_z,
+                   int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
+                   int64_t v0, int64_t v1, int32_t precision, float* out, void* stream);
+
+/* Paired / broadcast forward.  Replaces NdfModel.forward (model.py:179-189):
+ * p_mu is (n_mu, 3) fp64 device, p_nu (n, 3); n_mu == 1 broadcasts. */
+int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int64_t n_mu,
+                     const double* p_nu, int64_t n, int32_t precision, float* out,
+                     void* stream);
+
+/* Batched multi-reference query (BASELINE config 3; the loop in
+ * service.matrix_reconstruct, service.py:97-125, batched): refs is (n_ref, 3)
+ * fp64 device; out is fp16 (n_ref rows of ld_out halfs), row r holds
+ * vertices [v0, v1) of ref r.  precision must be NDF_PREC_BF16. */
+int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs, int32_t n_ref,
+                         int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
+                         int64_t v0, int64_t v1, uint16_t* out_f16, int64_t ld_out,
+                         void* stream);
+
+/* ---- ground-truth estimators -------------------------------------------- */
+
+/* Trilinear fp64 sampling of all members at B positions.
+ * Replaces ensemble.sample_many (ensemble.py:130-167); X is one variable's
+ * member-major (M, nz, ny, nx) fp32 block; out is (B, M) fp64. */
+int ndf_sample_many(const float* X, int32_t M, int32_t nx, int32_t ny, int32_t nz,
+                    const double* pos, int64_t B, double* out, void* stream);
+
+/* Per-vertex standardisation (one-time prep of the Pearson GEMV):
+ * Z[m][v] = (X[m][v] - mean_v) / sqrt(sum_m (X - mean_v)^2) in fp64 -> fp32;
+ * norm[v] = that sqrt (0 marks a degenerate vertex).  Vertices [v0, v1). */
+int ndf_zscore(const float* X, int32_t M, int64_t V, int64_t v0, int64_t v1,
+               float* Z, float* norm, void* stream);
+
+/* r[v] = sum_m Z[m][v] * z_ref[m] for v in [v0, v1), clipped to [-1, 1];
+ * rows equal to z_ref -> exactly 1.0; degenerate (norm[v]==0 or ref_degenerate)
+ * -> NaN.  Replaces measures.pearson_against (measures.py:84-108) over a
+ * node-aligned ground_truth_field (measures.py:286-295). */
+int ndf_pearson_gemv(const float* Z, const float* norm, int32_t M, int64_t V,
+                     const float* z_ref, int32_t ref_degenerate, int64_t v0, int64_t v1,
+                     float* out, void* stream);
+
+/* Row-wise Pearson of fp64 rows: a is (B, M) or (1, M) when a_stride == 0,
+ * b is (B, M); out (B,) fp64, NaN for degenerate rows, equal rows -> 1.0.
+ * Replaces measures.pearson_rowwise (measures.py:111-133) and
+ * pearson_against on sampled rows. */
+int ndf_pearson_rows(const double* a, int64_t a_stride, const double* b, int32_t M,
+                     int64_t B, double* out, void* stream);
+
+/* Member-major (M, V) -> vertex-major (V, M) copy of one variable (layout for
+ * pair lists). */
+int ndf_vertex_major(const float* X, int32_t M, int64_t V, float* Xv, void* stream);
+
+/* Pearson of vertex pairs (BASELINE config 4) from the vertex-major copy Xv:
+ * out[p] = pearson(Xv[pa[p], :], Xv[pb[p], :]) in fp64 (NaN if degenerate).
+ * Replaces the per-pair pearson_rowwise of training._targets (training.py:111-119). */
+int ndf_pearson_pairs(const float* Xv, int32_t M, int64_t V, const int64_t* pa,
+                      const int64_t* pb, int64_t n, double* out, void* stream);
+
+/* KSG mutual information (variant 1, max-norm), measures.py:173-203.
+ * jitter_r: (M,) fp64 = default_rng(0x5D17E3).random(M) - 0.5 (measures.py:168-170)
+ * psi_tab:  (M,) fp64, psi_tab[n] = digamma(n + 1) (measures.py:136-165)
+ * psi_k_plus_psi_m = digamma(k) + digamma(M)
+ * Outputs: mi (n,) fp64 (may be NULL) and/or mi_f32 (n,) (may be NULL);
+ * counts (n, 2, M) int32 n_x / n_y (may be NULL); *status_out (device int32)
+ * receives 1 if any count was -1 (the reference raises there).
+ *
+ * ndf_ksg_ref_nodes: a = ref_vec (M,) fp64 device; b = X[:, v] for v in [v0, v1)
+ *   (ground_truth_field(ksg_mi) over node positions, measures.py:296-314).
+ * ndf_ksg_rows: a = A rows (stride a_stride, 0 = broadcast), b = B rows (fp64).
+ * ndf_ksg_pairs: a = Xv[pa[p], :], b = Xv[pb[p], :] on the vertex-major copy
+ *   (BASELINE config 4). */
+int ndf_ksg_ref_nodes(const float* X, int32_t M, int64_t V, const double* ref_vec,
+                      int64_t v0, int64_t v1, int32_t k, const double* jitter_r,
+                      const double* psi_tab, double psi_k_plus_psi_m, double* mi,
+                      float* mi_f32, int32_t* counts, int32_t* status_out, void* stream);
+int ndf_ksg_rows(const double* a, int64_t a_stride, const double* b, int32_t M, int64_t B,
+                 int32_t k, const double* jitter_r, const double* psi_tab,
+                 double psi_k_plus_psi_m, double* mi, float* mi_f32, int32_t* counts,
+                 int32_t* status_out, void* stream);
+int ndf_ksg_pairs(const float* Xv, int32_t M, int64_t V, const int64_t* pa,
+                  const int64_t* pb, int64_t n, int32_t k, const double* jitter_r,
+                  const double* psi_tab, double psi_k_plus_psi_m, double* mi,
+                  float* mi_f32, int32_t* counts, int32_t* status_out, void* stream);
+
+/* ---- utilities ------------------------------------------------------------ */
+
+/* Number of kernel launches this library issued on the calling thread since
+ * the last reset (bench.py's gpu_launches claim). */
+int64_t ndf_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NDF_B200_H */

@@ -1,0 +1,46 @@
+// C-ABI plumbing: thread-local last error, launch counter, device queries.
+#include <atomic>
+#include <string>
+
+#include "ndf_common.cuh"
+
+namespace ndf {
+
+static thread_local std::string g_last_error;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+int sm_count() {
+  static thread_local int cached_dev = -1;
+  static thread_local int cached = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cached;
+  if (dev != cached_dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+}  // namespace ndf
+
+extern "C" int32_t ndf_abi_version(void) { return NDF_ABI_VERSION; }
+
+extern "C" const char* ndf_last_error(void) { return ndf::g_last_error.c_str(); }
+
+extern "C" int32_t ndf_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+extern "C" int64_t ndf_launch_count(int32_t reset) {
+  const int64_t n = ndf::g_launches;
+  if (reset) ndf::g_launches = 0;
+  return n;
+}

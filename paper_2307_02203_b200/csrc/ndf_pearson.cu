@@ -1,0 +1,356 @@
+// Ground-truth Pearson field (K3) + ensemble sampling / layout support (K5).
+//
+// Reference: measures.pearson_against (measures.py:84-108), pearson_rowwise
+// (measures.py:111-133), ground_truth_field's Pearson branch (measures.py:286-295),
+// sample_many (ensemble.py:130-167).
+//
+// Node-aligned fields use a one-time standardisation Z = (X - mean)/||X - mean||
+// (fp64 statistics, fp32 storage) and then an HBM-streaming GEMV r = Z^T z_ref:
+// each thread owns 4 consecutive vertices (one LDG.128 per member row, coalesced
+// across the warp), partial sums are kept in fp32 for 32 members and folded into
+// fp64 so the result stays within ~1e-7 of the reference's fp64 two-pass formula.
+#include <algorithm>
+
+#include "ndf_common.cuh"
+
+namespace ndf {
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+// ---- sample_many: ensemble.py:130-167 --------------------------------------
+// out[b][m] = sum over (dz, dy, dx) of (wz*wy*wx) * X[m, iz+dz, iy+dy, ix+dx],
+// accumulated from 0 in that loop order in fp64 (no FMA) -- bit-identical.
+__device__ __forceinline__ void frac_index(double p, int n, int& i0, double& t) {
+  double pc = fmin(fmax(p, -1.0), 1.0);
+  double u = dmul(dmul(dadd(pc, 1.0), 0.5), (double)(n - 1));
+  int i = (int)floor(u);
+  if (i < 0) i = 0;
+  if (i > n - 2) i = n - 2;
+  t = dsub(u, (double)i);
+  if (t < 1e-9) t = 0.0;
+  if (t > 1.0 - 1e-9) t = 1.0;
+  i0 = i;
+}
+
+__global__ void sample_many_kernel(const float* __restrict__ X, int M, int nx, int ny, int nz,
+                                   const double* __restrict__ pos, int64_t B,
+                                   double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * (int64_t)M) return;
+  const int64_t b = idx / M;
+  const int m = (int)(idx - b * M);
+  int ix, iy, iz;
+  double tx, ty, tz;
+  frac_index(pos[3 * b + 0], nx, ix, tx);
+  frac_index(pos[3 * b + 1], ny, iy, ty);
+  frac_index(pos[3 * b + 2], nz, iz, tz);
+  const int64_t V = (int64_t)nx * ny * nz;
+  const float* g = X + (int64_t)m * V;
+  double acc = 0.0;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    const double wz = dz ? tz : dsub(1.0, tz);
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const double wy = dy ? ty : dsub(1.0, ty);
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const double wx = dx ? tx : dsub(1.0, tx);
+        const double w = dmul(dmul(wz, wy), wx);
+        const float c = g[(int64_t)(iz + dz) * ny * nx + (int64_t)(iy + dy) * nx + (ix + dx)];
+        acc = dadd(acc, dmul(w, (double)c));
+      }
+    }
+  }
+  out[idx] = acc;
+}
+
+// ---- z-score prep -----------------------------------------------------------
+__global__ void zscore_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0,
+                              int64_t v1, float* __restrict__ Z, float* __restrict__ norm) {
+  const int64_t v = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= v1) return;
+  const float* col = X + v;
+  const double K = (double)col[0];
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
+  for (int m = 0; m < M; ++m) {
+    const double d = (double)__ldg(col + (int64_t)m * V) - K;
+    s1 += d;
+    s2 += d * d;
+  }
+  const double off = s1 / (double)M;
+  double var = s2 - s1 * off;
+  if (!(var > 0.0)) {
+    for (int m = 0; m < M; ++m) Z[(int64_t)m * V + v] = 0.0f;
+    if (norm) norm[v] = 0.0f;
+    return;
+  }
+  const double mu = K + off;
+  const double inv = 1.0 / sqrt(var);
+#pragma unroll 8
+  for (int m = 0; m < M; ++m)
+    Z[(int64_t)m * V + v] = (float)(((double)__ldg(col + (int64_t)m * V) - mu) * inv);
+  if (norm) norm[v] = (float)sqrt(var);
+}
+
+// ---- Pearson GEMV over Z -----------------------------------------------------
+template <bool kVec>
+__global__ void __launch_bounds__(256)
+gemv_kernel(const float* __restrict__ Z, const float* __restrict__ norm, int M, int64_t V,
+            const float* __restrict__ zref, int ref_deg, int64_t v0, int64_t v1,
+            float* __restrict__ out) {
+  extern __shared__ float zr[];
+  for (int i = threadIdx.x; i < M; i += blockDim.x) zr[i] = zref[i];
+  __syncthreads();
+  const int64_t v = v0 + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (v >= v1) return;
+  double tot[4] = {0.0, 0.0, 0.0, 0.0};
+  bool eq[4] = {true, true, true, true};
+  if (kVec) {
+    const float* zp = Z + v;
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m1 = min(M, m0 + 32);
+      float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll 8
+      for (int m = m0; m < m1; ++m) {
+        const float4 z = ld_stream4(zp + (int64_t)m * V);
+        const float r = zr[m];
+        p0 = fmaf(z.x, r, p0); p1 = fmaf(z.y, r, p1);
+        p2 = fmaf(z.z, r, p2); p3 = fmaf(z.w, r, p3);
+        eq[0] &= (z.x == r); eq[1] &= (z.y == r); eq[2] &= (z.z == r); eq[3] &= (z.w == r);
+      }
+      tot[0] += p0; tot[1] += p1; tot[2] += p2; tot[3] += p3;
+    }
+  } else {
+    for (int i = 0; i < 4; ++i) {
+      if (v + i >= v1) break;
+      const float* zp = Z + v + i;
+      for (int m0 = 0; m0 < M; m0 += 32) {
+        const int m1 = min(M, m0 + 32);
+        float p = 0.f;
+        for (int m = m0; m < m1; ++m) {
+          const float z = __ldg(zp + (int64_t)m * V);
+          p = fmaf(z, zr[m], p);
+          eq[i] &= (z == zr[m]);
+        }
+        tot[i] += p;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (v + i >= v1) break;
+    float r;
+    if (ref_deg || norm[v + i] == 0.0f) {
+      r = __int_as_float(0x7fc00000);   // NaN: degenerate (measures.py:94-100)
+    } else if (eq[i]) {
+      r = 1.0f;                          // measures.py:102-107
+    } else {
+      r = (float)fmin(1.0, fmax(-1.0, tot[i]));
+    }
+    out[v + i - v0] = r;
+  }
+}
+
+// ---- Pearson of fp64 rows (pearson_rowwise / pearson_against) ----------------
+__global__ void pearson_rows_kernel(const double* __restrict__ a, int64_t a_stride,
+                                    const double* __restrict__ b, int M, int64_t B,
+                                    double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= B) return;
+  const double* ar = a + row * a_stride;
+  const double* br = b + row * (int64_t)M;
+  double sa = 0.0, sb = 0.0;
+  for (int m = lane; m < M; m += 32) { sa += ar[m]; sb += br[m]; }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  const double ma = sa / M, mb = sb / M;
+  double saa = 0.0, sbb = 0.0, sab = 0.0;
+  int eq = 1;
+  for (int m = lane; m < M; m += 32) {
+    const double x = ar[m] - ma, y = br[m] - mb;
+    saa += x * x; sbb += y * y; sab += x * y;
+    eq &= (ar[m] == br[m]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    saa += __shfl_xor_sync(0xffffffffu, saa, o);
+    sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+    sab += __shfl_xor_sync(0xffffffffu, sab, o);
+  }
+  eq = __all_sync(0xffffffffu, eq);
+  if (lane == 0) {
+    double r;
+    if (!(saa > 0.0) || !(sbb > 0.0)) {
+      r = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      r = sab / sqrt(saa * sbb);
+      r = fmin(1.0, fmax(-1.0, r));
+      if (eq && r > 1.0 - 1e-9) r = 1.0;
+    }
+    out[row] = r;
+  }
+}
+
+// ---- Pearson of vertex pairs from the vertex-major copy ------------------------
+__global__ void pearson_pairs_kernel(const float* __restrict__ Xv, int M,
+                                     const int64_t* __restrict__ pa,
+                                     const int64_t* __restrict__ pb, int64_t n,
+                                     double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const float* ar = Xv + pa[p] * (int64_t)M;
+  const float* br = Xv + pb[p] * (int64_t)M;
+  double sa = 0.0, sb = 0.0;
+  for (int m = lane; m < M; m += 32) { sa += ar[m]; sb += br[m]; }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  const double ma = sa / M, mb = sb / M;
+  double saa = 0.0, sbb = 0.0, sab = 0.0;
+  int eq = 1;
+  for (int m = lane; m < M; m += 32) {
+    const double x = (double)ar[m] - ma, y = (double)br[m] - mb;
+    saa += x * x; sbb += y * y; sab += x * y;
+    eq &= (ar[m] == br[m]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    saa += __shfl_xor_sync(0xffffffffu, saa, o);
+    sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+    sab += __shfl_xor_sync(0xffffffffu, sab, o);
+  }
+  eq = __all_sync(0xffffffffu, eq);
+  if (lane == 0) {
+    double r;
+    if (!(saa > 0.0) || !(sbb > 0.0)) {
+      r = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      r = fmin(1.0, fmax(-1.0, sab / sqrt(saa * sbb)));
+      if (eq && r > 1.0 - 1e-9) r = 1.0;
+    }
+    out[p] = r;
+  }
+}
+
+// ---- member-major -> vertex-major transpose (K5) -----------------------------
+__global__ void transpose_kernel(const float* __restrict__ X, int M, int64_t V,
+                                 float* __restrict__ Xv) {
+  __shared__ float tile[32][33];
+  const int64_t vb = (int64_t)blockIdx.x * 32;
+  const int mb = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int m = mb + r;
+    const int64_t v = vb + threadIdx.x;
+    if (m < M && v < V) tile[r][threadIdx.x] = X[(int64_t)m * V + v];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t v = vb + r;
+    const int m = mb + threadIdx.x;
+    if (m < M && v < V) Xv[v * M + m] = tile[threadIdx.x][r];
+  }
+}
+
+}  // namespace ndf
+
+using namespace ndf;
+
+extern "C" int ndf_sample_many(const float* X, int32_t M, int32_t nx, int32_t ny, int32_t nz,
+                               const double* pos, int64_t B, double* out, void* stream) {
+  NDF_REQUIRE(M >= 1 && nx >= 2 && ny >= 2 && nz >= 2, NDF_ERR_PARAMETER,
+              "sample_many: need M >= 1 and >= 2 nodes per axis");
+  NDF_REQUIRE(B >= 0, NDF_ERR_PARAMETER, "negative batch");
+  if (B == 0) return NDF_OK;
+  NDF_REQUIRE(X && pos && out, NDF_ERR_PARAMETER, "null pointer");
+  const int64_t n = B * (int64_t)M;
+  const int threads = 256;
+  sample_many_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+      X, M, nx, ny, nz, pos, B, out);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_zscore(const float* X, int32_t M, int64_t V, int64_t v0, int64_t v1,
+                          float* Z, float* norm, void* stream) {
+  NDF_REQUIRE(M >= 1 && V >= 1, NDF_ERR_PARAMETER, "zscore: empty ensemble");
+  NDF_REQUIRE(v0 >= 0 && v0 <= v1 && v1 <= V, NDF_ERR_PARAMETER, "vertex range out of bounds");
+  if (v0 == v1) return NDF_OK;
+  NDF_REQUIRE(X && Z, NDF_ERR_PARAMETER, "null pointer");
+  const int threads = 256;
+  zscore_kernel<<<(unsigned)((v1 - v0 + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+      X, M, V, v0, v1, Z, norm);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_pearson_gemv(const float* Z, const float* norm, int32_t M, int64_t V,
+                                const float* z_ref, int32_t ref_degenerate, int64_t v0,
+                                int64_t v1, float* out, void* stream) {
+  NDF_REQUIRE(M >= 1 && M <= 12288, NDF_ERR_UNSUPPORTED, "pearson_gemv: M must be in [1, 12288]");
+  NDF_REQUIRE(v0 >= 0 && v0 <= v1 && v1 <= V, NDF_ERR_PARAMETER, "vertex range out of bounds");
+  if (v0 == v1) return NDF_OK;
+  NDF_REQUIRE(Z && norm && z_ref && out, NDF_ERR_PARAMETER, "null pointer");
+  const int threads = 256;
+  const int64_t nthreads = (v1 - v0 + 3) / 4;
+  const unsigned blocks = (unsigned)((nthreads + threads - 1) / threads);
+  const size_t smem = sizeof(float) * M;
+  const bool vec = (V % 4 == 0) && (v0 % 4 == 0) && ((reinterpret_cast<uintptr_t>(Z) & 15) == 0);
+  if (vec)
+    gemv_kernel<true><<<blocks, threads, smem, as_stream(stream)>>>(Z, norm, M, V, z_ref,
+                                                                    ref_degenerate, v0, v1, out);
+  else
+    gemv_kernel<false><<<blocks, threads, smem, as_stream(stream)>>>(Z, norm, M, V, z_ref,
+                                                                     ref_degenerate, v0, v1, out);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_pearson_rows(const double* a, int64_t a_stride, const double* b, int32_t M,
+                                int64_t B, double* out, void* stream) {
+  NDF_REQUIRE(M >= 2, NDF_ERR_PARAMETER, "need at least two samples");
+  NDF_REQUIRE(B >= 0, NDF_ERR_PARAMETER, "negative batch");
+  if (B == 0) return NDF_OK;
+  NDF_REQUIRE(a && b && out, NDF_ERR_PARAMETER, "null pointer");
+  const int threads = 256;
+  pearson_rows_kernel<<<(unsigned)((B * 32 + threads - 1) / threads), threads, 0,
+                        as_stream(stream)>>>(a, a_stride, b, M, B, out);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_pearson_pairs(const float* Xv, int32_t M, int64_t V, const int64_t* pa,
+                                 const int64_t* pb, int64_t n, double* out, void* stream) {
+  NDF_REQUIRE(M >= 2, NDF_ERR_PARAMETER, "need at least two samples");
+  NDF_REQUIRE(n >= 0 && V >= 1, NDF_ERR_PARAMETER, "bad sizes");
+  if (n == 0) return NDF_OK;
+  NDF_REQUIRE(Xv && pa && pb && out, NDF_ERR_PARAMETER, "null pointer");
+  const int threads = 256;
+  pearson_pairs_kernel<<<(unsigned)((n * 32 + threads - 1) / threads), threads, 0,
+                         as_stream(stream)>>>(Xv, M, pa, pb, n, out);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_vertex_major(const float* X, int32_t M, int64_t V, float* Xv, void* stream) {
+  NDF_REQUIRE(M >= 1 && V >= 1, NDF_ERR_PARAMETER, "empty ensemble");
+  NDF_REQUIRE(X && Xv, NDF_ERR_PARAMETER, "null pointer");
+  NDF_REQUIRE(M <= 65535 * 32, NDF_ERR_UNSUPPORTED, "too many members");
+  dim3 grid((unsigned)((V + 31) / 32), (unsigned)((M + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(X, M, V, Xv);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}

@@ -1,0 +1,277 @@
+"""Ensemble containers, NDFE IO and GPU-resident ensembles.
+
+Mirrors the reference's ``ensemble.py`` (GridDomain ``:34-62``, EnsembleField
+``:65-112``, NDFE ``save_ensemble``/``load_ensemble`` ``:283-333``,
+``sample_many``/``sample_at`` ``:130-173``) with the same semantics, plus
+``DeviceEnsemble``: one variable's member-major fp32 block resident in HBM
+(the NDFE payload layout, ``(M, nz, ny, nx)``), with lazily built derived
+layouts (standardised Z for the Pearson GEMV, vertex-major copy for pair lists).
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import (CorruptFileError, DataError, FormatError, ParameterError,
+                     UnknownVariableError)
+
+NDFE_MAGIC = b"NDFE"
+NDFE_VERSION = 1
+
+
+@dataclass(frozen=True)
+class GridDomain:
+    """Node counts of a regular grid over Omega = [-1, 1]^3 (ensemble.py:34-62)."""
+
+    nx: int
+    ny: int
+    nz: int
+
+    def __post_init__(self):
+        for n in (self.nx, self.ny, self.nz):
+            if int(n) != n or n < 2:
+                raise ParameterError(f"grid axes need >= 2 nodes, got {self!r}")
+
+    @property
+    def node_count(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    @property
+    def dims(self):
+        return (self.nx, self.ny, self.nz)
+
+    def axis_coords(self, axis: int) -> np.ndarray:
+        n = (self.nx, self.ny, self.nz)[axis]
+        return 2.0 * np.arange(n) / (n - 1) - 1.0
+
+    def node_positions(self) -> np.ndarray:
+        zs, ys, xs = np.meshgrid(self.axis_coords(2), self.axis_coords(1),
+                                 self.axis_coords(0), indexing="ij")
+        return np.column_stack([xs.ravel(), ys.ravel(), zs.ravel()])
+
+
+@dataclass(frozen=True)
+class EnsembleField:
+    """N member grids per variable, float32 (d, N, nz, ny, nx) (ensemble.py:65-112)."""
+
+    domain: GridDomain
+    variables: tuple
+    values: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        vals = np.asarray(self.values, dtype=np.float32)
+        object.__setattr__(self, "values", vals)
+        object.__setattr__(self, "variables", tuple(self.variables))
+        if len(set(self.variables)) != len(self.variables):
+            raise DataError(f"duplicate variable names: {self.variables}")
+        if vals.ndim != 5:
+            raise DataError(f"values must be (d, N, nz, ny, nx), got {vals.shape}")
+        d, n, nz, ny, nx = vals.shape
+        if d != len(self.variables):
+            raise DataError(f"{len(self.variables)} variable names but {d} value blocks")
+        if (nx, ny, nz) != (self.domain.nx, self.domain.ny, self.domain.nz):
+            raise DataError(f"grid shape {(nx, ny, nz)} does not match domain {self.domain}")
+        if n < 1:
+            raise DataError("ensemble needs at least one member")
+        if not np.isfinite(vals).all():
+            raise DataError("ensemble contains non-finite values")
+        object.__setattr__(self, "_device_cache", {})
+
+    @property
+    def member_count(self) -> int:
+        return self.values.shape[1]
+
+    def variable_index(self, name: str) -> int:
+        try:
+            return self.variables.index(name)
+        except ValueError:
+            raise UnknownVariableError(
+                f"unknown variable {name!r}; have {list(self.variables)}") from None
+
+    def member_grids(self, name: str) -> np.ndarray:
+        return self.values[self.variable_index(name)]
+
+    def to_device(self, variable: str, device=None) -> "DeviceEnsemble":
+        """Upload one variable once (cached per device): the HBM-resident copy."""
+        dev = N.require_cuda(device)
+        key = (variable, str(dev))
+        cache = self._device_cache
+        if key not in cache:
+            cache[key] = DeviceEnsemble.from_numpy(self.member_grids(variable), device=dev)
+        return cache[key]
+
+
+class DeviceEnsemble:
+    """One variable's ensemble resident on a CUDA device, member-major fp32.
+
+    ``X`` is a torch tensor of shape (M, nz, ny, nx) -- the NDFE payload layout,
+    so member rows are contiguous over vertices (coalesced GEMV / KSG loads).
+    """
+
+    def __init__(self, X, domain: GridDomain):
+        import torch
+        if X.dtype != torch.float32 or X.dim() != 4 or not X.is_cuda:
+            raise DataError("DeviceEnsemble needs a (M, nz, ny, nx) float32 CUDA tensor")
+        M, nz, ny, nx = X.shape
+        if (nx, ny, nz) != domain.dims:
+            raise DataError("tensor shape does not match domain")
+        self.X = X.contiguous()
+        self.domain = domain
+        self._z = None
+        self._norm = None
+        self._xv = None
+
+    @classmethod
+    def from_numpy(cls, grids: np.ndarray, device=None) -> "DeviceEnsemble":
+        import torch
+        dev = N.require_cuda(device)
+        g = np.ascontiguousarray(grids, dtype=np.float32)
+        if g.ndim != 4:
+            raise DataError("member grids must be (N, nz, ny, nx)")
+        t = torch.from_numpy(g).to(dev, non_blocking=False)
+        return cls(t, GridDomain(g.shape[3], g.shape[2], g.shape[1]))
+
+    @property
+    def member_count(self) -> int:
+        return int(self.X.shape[0])
+
+    @property
+    def node_count(self) -> int:
+        return self.domain.node_count
+
+    @property
+    def device(self):
+        return self.X.device
+
+    def zscore(self):
+        """(Z, norm): standardised copy for the Pearson GEMV, built once (ndf_zscore)."""
+        import torch
+        if self._z is None:
+            M, V = self.member_count, self.node_count
+            Z = torch.empty((M, V), dtype=torch.float32, device=self.device)
+            norm = torch.empty((V,), dtype=torch.float32, device=self.device)
+            N.call("ndf_zscore", N.ptr(self.X), M, V, 0, V, N.ptr(Z), N.ptr(norm),
+                   N.stream_handle(self.device))
+            self._z, self._norm = Z, norm
+        return self._z, self._norm
+
+    def vertex_major(self):
+        """(V, M) copy for pair lists, built once (ndf_vertex_major)."""
+        import torch
+        if self._xv is None:
+            M, V = self.member_count, self.node_count
+            Xv = torch.empty((V, M), dtype=torch.float32, device=self.device)
+            N.call("ndf_vertex_major", N.ptr(self.X), M, V, N.ptr(Xv), N.stream_handle(self.device))
+            self._xv = Xv
+        return self._xv
+
+    def drop_derived(self):
+        self._z = self._norm = self._xv = None
+
+    def sample_many(self, positions) -> "torch.Tensor":
+        """Trilinear fp64 samples (B, M) on device (ndf_sample_many)."""
+        import torch
+        pos = _as_device_positions(positions, self.device)
+        B = int(pos.shape[0])
+        out = torch.empty((B, self.member_count), dtype=torch.float64, device=self.device)
+        d = self.domain
+        N.call("ndf_sample_many", N.ptr(self.X), self.member_count, d.nx, d.ny, d.nz, N.ptr(pos), B,
+               N.ptr(out), N.stream_handle(self.device))
+        return out
+
+
+def _as_device_positions(positions, device):
+    import torch
+    if isinstance(positions, torch.Tensor):
+        pos = positions.to(device=device, dtype=torch.float64)
+    else:
+        pos = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(
+            np.asarray(positions, dtype=np.float64)))).to(device)
+    if pos.dim() != 2 or pos.shape[1] != 3:
+        raise ParameterError(f"positions must be (M, 3), got {tuple(pos.shape)}")
+    return pos.contiguous()
+
+
+def _device_view(field_obj, variable: str, device=None) -> DeviceEnsemble:
+    if isinstance(field_obj, DeviceEnsemble):
+        return field_obj
+    if isinstance(field_obj, dict):          # {name: DeviceEnsemble}
+        try:
+            return field_obj[variable]
+        except KeyError:
+            raise UnknownVariableError(f"unknown variable {variable!r}") from None
+    return field_obj.to_device(variable, device)
+
+
+def sample_many(field_obj, variable: str, positions, chunk: int = 8192) -> np.ndarray:
+    """ensemble.py:130-167 on the GPU (fp64 trilinear, bit-identical); returns (M, N) fp64."""
+    dev = _device_view(field_obj, variable)
+    pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+    if pos.ndim != 2 or pos.shape[1] != 3:
+        raise ParameterError(f"positions must be (M, 3), got {pos.shape}")
+    return dev.sample_many(pos).cpu().numpy()
+
+
+def sample_at(field_obj, variable: str, position) -> np.ndarray:
+    """ensemble.py:170-173."""
+    return sample_many(field_obj, variable,
+                       np.asarray(position, dtype=np.float64).reshape(1, 3))[0]
+
+
+# ---------------------------------------------------------------------------
+# NDFE container (ensemble.py:283-333), byte-compatible with the reference
+
+
+def save_ensemble(field_obj: EnsembleField, path) -> None:
+    dom = field_obj.domain
+    with open(path, "wb") as fh:
+        fh.write(NDFE_MAGIC)
+        fh.write(struct.pack("<6I", NDFE_VERSION, dom.nx, dom.ny, dom.nz,
+                             field_obj.member_count, len(field_obj.variables)))
+        for name in field_obj.variables:
+            raw = name.encode("utf-8")
+            fh.write(struct.pack("<H", len(raw)))
+            fh.write(raw)
+        fh.write(np.ascontiguousarray(field_obj.values, dtype="<f4").tobytes())
+
+
+def load_ensemble(path) -> EnsembleField:
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != NDFE_MAGIC:
+            raise FormatError(f"bad magic {magic!r}, expected {NDFE_MAGIC!r}")
+        head = fh.read(24)
+        if len(head) != 24:
+            raise CorruptFileError("truncated header")
+        version, nx, ny, nz, n, d = struct.unpack("<6I", head)
+        if version != NDFE_VERSION:
+            raise FormatError(f"unsupported NDFE version {version}")
+        names = []
+        for _ in range(d):
+            raw_len = fh.read(2)
+            if len(raw_len) != 2:
+                raise CorruptFileError("truncated variable table")
+            (name_len,) = struct.unpack("<H", raw_len)
+            raw = fh.read(name_len)
+            if len(raw) != name_len:
+                raise CorruptFileError("truncated variable name")
+            names.append(raw.decode("utf-8"))
+        expected = d * n * nz * ny * nx
+        payload = fh.read()
+        if len(payload) != expected * 4:
+            raise CorruptFileError(
+                f"payload holds {len(payload) // 4} float32 values, expected {expected}")
+    values = np.frombuffer(payload, dtype="<f4").reshape(d, n, nz, ny, nx)
+    if not np.isfinite(values).all():
+        raise DataError("ensemble file contains non-finite values")
+    try:
+        domain = GridDomain(nx, ny, nz)
+    except ParameterError as exc:
+        raise CorruptFileError(str(exc)) from exc
+    # the reference copies the payload (ensemble.py:333); frombuffer is read-only
+    # and EnsembleField is immutable, so the zero-copy view is safe here.
+    return EnsembleField(domain, tuple(names), values)

@@ -1,0 +1,193 @@
+"""GPU parity of the NDF query (K1+K2) against the oracle and the reference's golden vectors.
+
+Tolerances (BASELINE north_star): fp32 path within 1e-5 absolute; bf16
+tensor-core path within 1e-2 absolute of the fp32 reference output.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2307_02203_b200 as ndf  # noqa: E402
+from oracle import ndf_oracle as O  # noqa: E402
+from paper_2307_02203_b200 import workloads as W  # noqa: E402
+
+TOL32 = 1e-5
+TOL16 = 1e-2
+
+
+def refmode_model(g, merge, precision):
+    grid = g[f"{merge}_grid"].reshape(4, 4, 4, 16)
+    spec = ndf.ModelSpec(merge=merge, fourier_octaves=6, features_per_level=16,
+                         grid_resolution=(4, 4, 4), activation="snake_alt", head="linear",
+                         precision=precision, channels=128, decoder_layers=4)
+    return ndf.NdfModel(spec, grid, grid, [g[f"{merge}_w{i}"] for i in range(4)],
+                        [g[f"{merge}_b{i}"] for i in range(4)])
+
+
+def oracle_model(model):
+    return O.OracleModel(model.spec.fourier_octaves, model.grid_mu, model.grid_nu, model.weights,
+                         model.biases, model.spec.merge, model.spec.activation,
+                         model.spec.head_kind)
+
+
+@pytest.mark.parametrize("merge", ["add", "absdiff", "multiply"])
+def test_reference_mode_golden_fp32(golden, merge):
+    """Unmodified-reference outputs (tests/golden/make_golden.py) reproduced in fp32."""
+    g = golden("ndf_refmode")
+    model = refmode_model(g, merge, "fp32")
+    dims = tuple(int(d) for d in g["dims"])
+    for r, ref in enumerate(g["refs"]):
+        got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
+        want = g[f"{merge}_out{r}"]
+        assert np.max(np.abs(got - want)) <= TOL32 * max(1.0, np.abs(want).max())
+    got = model.forward(g[f"{merge}_p1"], g[f"{merge}_p2"])
+    want = g[f"{merge}_fwd"]
+    assert np.max(np.abs(got - want)) <= TOL32 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("merge", ["add", "absdiff", "multiply"])
+def test_reference_mode_golden_bf16(golden, merge):
+    g = golden("ndf_refmode")
+    model = refmode_model(g, merge, "bf16")
+    dims = tuple(int(d) for d in g["dims"])
+    for r, ref in enumerate(g["refs"]):
+        got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
+        want = g[f"{merge}_out{r}"]
+        # linear head, unbounded output: 1e-2 relative to the output scale
+        assert np.max(np.abs(got - want)) <= TOL16 * max(1.0, np.abs(want).max())
+    got = model.forward(g[f"{merge}_p1"], g[f"{merge}_p2"])
+    want = g[f"{merge}_fwd"]
+    assert np.max(np.abs(got - want)) <= TOL16 * max(1.0, np.abs(want).max())
+
+
+@pytest.fixture(scope="module")
+def c0():
+    w = W.CONFIGS[0]
+    model = W.build_model(w, seed=0, grid_init=1.0)
+    rng = np.random.default_rng(17)
+    for b in model.biases:        # non-zero biases so bias handling is checked
+        b[:] = rng.uniform(-0.3, 0.3, b.shape).astype(np.float32)
+    return w, model
+
+
+@pytest.mark.parametrize("head", ["tanh", "softplus"])
+def test_c0_fp32_and_bf16(c0, head):
+    w, base = c0
+    from dataclasses import replace
+    model = ndf.NdfModel(replace(base.spec, head=head), base.grid_mu, base.grid_nu, base.weights,
+                         base.biases)
+    ref = w.ref_position()
+    want = O.reconstruct_field(oracle_model(model), ref, w.dims)
+    got32 = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims).values
+    got16 = ndf.reconstruct_field(model.with_precision("bf16"), ref, ndf.ROLE_MU, w.dims).values
+    e32 = np.max(np.abs(got32 - want))
+    e16 = np.max(np.abs(got16 - want))
+    print(f"c0 {head}: fp32 max|err| {e32:.3e}  bf16 max|err| {e16:.3e}")
+    assert e32 <= TOL32
+    assert e16 <= TOL16
+
+
+def test_c0_off_node_ref_and_other_dims(c0):
+    w, model = c0
+    for ref, dims in [((0.123, -0.77, 0.5), w.dims), ((1.3, -2.0, 0.0), (17, 9, 5)),
+                      ((0.0, 0.0, 0.0), (1, 1, 1)), ((-0.4, 0.9, -0.1), (33, 1, 7))]:
+        want = O.reconstruct_field(oracle_model(model), ref, dims)
+        got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
+        assert np.max(np.abs(got - want)) <= TOL32
+        got16 = ndf.reconstruct_field(model.with_precision("bf16"), ref, ndf.ROLE_MU, dims).values
+        assert np.max(np.abs(got16 - want)) <= TOL16
+
+
+def test_role_swap_and_symmetry(c0):
+    w, model = c0
+    ref = (0.3, -0.2, 0.1)
+    for prec in ("fp32", "bf16"):
+        m = model.with_precision(prec)
+        a = ndf.reconstruct_field(m, ref, ndf.ROLE_MU, (9, 7, 5)).values
+        b = ndf.reconstruct_field(m, ref, ndf.ROLE_NU, (9, 7, 5)).values
+        assert np.array_equal(a, b)     # shared model + symmetric merge: exact
+        rng = np.random.default_rng(3)
+        p1 = rng.uniform(-1, 1, (300, 3))
+        p2 = rng.uniform(-1, 1, (300, 3))
+        assert np.array_equal(m.forward(p1, p2), m.forward(p2, p1))
+
+
+def test_batch_invariance_and_vertex_ranges(c0):
+    """reference tests/test_service.py:42-54: batched == looped, bitwise."""
+    w, model = c0
+    ref = w.ref_position()
+    for prec in ("fp32", "bf16"):
+        m = model.with_precision(prec)
+        full = ndf.reconstruct_field_device(m, ref, ndf.ROLE_MU, w.dims).cpu().numpy()
+        parts = [ndf.reconstruct_field_device(m, ref, ndf.ROLE_MU, w.dims, v0, v1).cpu().numpy()
+                 for v0, v1 in [(0, 1), (1, 1000), (1000, 1001), (1001, w.n_vertices)]]
+        assert np.array_equal(np.concatenate(parts), full)
+        pos = O.grid_positions(w.dims)[:50]
+        looped = np.array([m.forward(np.asarray(ref).reshape(1, 3), pos[i:i + 1])[0]
+                           for i in range(50)])
+        assert np.array_equal(looped, full[:50])
+
+
+def test_constant_decoder_bias():
+    """reference tests/test_model.py:99-109."""
+    spec = ndf.ModelSpec(grid_resolution=(3, 3, 3), head="linear")
+    model = ndf.NdfModel.build(spec, seed=3)
+    for wt in model.weights:
+        wt[:] = 0.0
+    for b in model.biases:
+        b[:] = 0.0
+    model.biases[-1][0] = 0.75
+    rng = np.random.default_rng(4)
+    for prec in ("fp32", "bf16"):
+        out = model.with_precision(prec).forward(rng.uniform(-1, 1, (16, 3)),
+                                                 rng.uniform(-1, 1, (16, 3)))
+        assert np.all(out == np.float32(0.75))
+
+
+def test_corrupt_model_rejected():
+    spec = ndf.ModelSpec(grid_resolution=(3, 3, 3))
+    model = ndf.NdfModel.build(spec, seed=7)
+    model.grid_mu[0, 0, 0, 0] = np.nan
+    with pytest.raises(ndf.ModelCorruptError):
+        model.forward(np.zeros((1, 3)), np.zeros((1, 3)))
+
+
+def test_invalid_role_and_shapes(c0):
+    _, model = c0
+    with pytest.raises(ndf.ParameterError):
+        ndf.reconstruct_field(model, (0, 0, 0), "reference-is-q", (4, 4, 4))
+    with pytest.raises(ndf.ShapeError):
+        model.forward(np.zeros((2, 2)), np.zeros((2, 3)))
+
+
+def test_clamp_limits_range(c0):
+    _, base = c0
+    from dataclasses import replace
+    model = ndf.NdfModel(replace(base.spec, head="linear"), base.grid_mu, base.grid_nu,
+                         base.weights, base.biases)
+    g = ndf.reconstruct_field(model, (0, 0, 0), ndf.ROLE_MU, (5, 5, 5), clamp=True)
+    assert g.values.min() >= -1.0 and g.values.max() <= 1.0
+
+
+def test_large_grid_bf16_vs_fp32():
+    """c1-shaped model on a 250x352x4 slab: bf16 tensor-core path vs exact fp32 path
+    (size-independent property at scale; the fp32 path is itself oracle-pinned)."""
+    w = W.CONFIGS[1]
+    model = W.build_model(w, seed=0, grid_init=1.0)
+    dims = (250, 352, 4)
+    ref = w.ref_position()
+    a = ndf.reconstruct_field_device(model.with_precision("fp32"), ref, ndf.ROLE_MU, dims)
+    b = ndf.reconstruct_field_device(model.with_precision("bf16"), ref, ndf.ROLE_MU, dims)
+    err = (a - b).abs().max().item()
+    print("250x352x4 bf16 vs fp32 max|err|", err)
+    assert err <= TOL16
+    # oracle spot check on a seeded vertex subset
+    idx = np.random.default_rng(5).integers(0, a.numel(), 2000)
+    want = O.reconstruct_field(oracle_model(model), ref, dims, vertices=idx)
+    assert np.max(np.abs(a.cpu().numpy()[idx] - want)) <= TOL32
