@@ -45,7 +45,8 @@ enum { NDF_ACT_RELU = 0, NDF_ACT_SNAKE = 1, NDF_ACT_SNAKE_ALT = 2, NDF_ACT_SILU 
 enum { NDF_HEAD_LINEAR = 0, NDF_HEAD_TANH = 1, NDF_HEAD_SOFTPLUS = 2 };
 /* query precision */
 enum { NDF_PREC_FP32 = 0,   /* SIMT fp32, sequential k-sum (nn.py:18-20 order) */
-       NDF_PREC_BF16 = 1 }; /* tcgen05 bf16 x bf16 -> fp32 TMEM accumulators */
+       NDF_PREC_BF16 = 1,   /* tcgen05 bf16 x bf16 -> fp32 TMEM accumulators */
+       NDF_PREC_FP16 = 2 }; /* tcgen05 fp16 x fp16 -> fp32 (same speed, 3 more mantissa bits) */
 
 /*
  * Model descriptor (host struct, device pointers inside).
@@ -61,6 +62,7 @@ typedef struct ndf_model_desc {
   int32_t head;                   /* NDF_HEAD_* */
   int32_t n_layers;               /* decoder affine layers incl. output layer */
   int32_t widths[NDF_MAX_LAYERS + 1]; /* decoder widths [in, h1, ..., 1] */
+  int32_t tc_format;              /* element type of params_tc: NDF_PREC_BF16 / NDF_PREC_FP16 */
   const float* grid_mu;           /* device (rz, ry, rx, C) fp32 */
   const float* grid_nu;           /* device; == grid_mu for shared models */
   const float* params_f32;        /* device: W0 (in x h1, row-major), b0, W1, b1, ...
@@ -79,7 +81,8 @@ int32_t ndf_device_sm_count(void);
  * model is outside the tcgen05 kernel's envelope: hidden width 128, input
  * width <= 128, >= 2 affine layers, output width 1). */
 size_t ndf_tc_blob_bytes(const ndf_model_desc* m);
-/* Pack params_f32 into the UMMA-canonical bf16 blob (device kernel).
+/* Pack params_f32 into the UMMA-canonical 16-bit blob of element type
+ * m->tc_format (device kernel).
  * Replaces nothing in the reference: it is the "validate once at upload"
  * step (failure detection). */
 int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_bytes, void* stream);
@@ -102,7 +105,7 @@ int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int64_t n_mu,
 /* Batched multi-reference query (BASELINE config 3; the loop in
  * service.matrix_reconstruct, service.py:97-125, batched): refs is (n_ref, 3)
  * fp64 device; out is fp16 (n_ref rows of ld_out halfs), row r holds
- * vertices [v0, v1) of ref r.  precision must be NDF_PREC_BF16. */
+ * vertices [v0, v1) of ref r.  precision must be NDF_PREC_BF16 or NDF_PREC_FP16. */
 int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs, int32_t n_ref,
                          int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
                          int64_t v0, int64_t v1, uint16_t* out_f16, int64_t ld_out,

@@ -49,6 +49,20 @@ def grid_positions(dims):
     return np.column_stack([xx.ravel(), yy.ravel(), zz.ravel()])
 
 
+def grid_positions_of(dims, vertices):
+    """Rows ``vertices`` of grid_positions(dims), without materialising the grid
+    (same per-axis formula, so the same bits)."""
+    def axis(n):
+        if n == 1:
+            return np.zeros(1)
+        return 2.0 * np.arange(n) / (n - 1) - 1.0
+
+    x, y, z = dims
+    v = np.asarray(vertices, dtype=np.int64)
+    ix, iy, iz = v % x, (v // x) % y, v // (x * y)
+    return np.column_stack([axis(x)[ix], axis(y)[iy], axis(z)[iz]])
+
+
 def fourier_encode(positions, L):
     """encoding.py:37-51 -- octave-major, axis-minor, sin before cos."""
     pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
@@ -241,9 +255,10 @@ def reconstruct_field(model: OracleModel, ref, dims, role="reference-is-mu",
     depend on the batch layout (nn.py:1-7).
     """
     ref = np.asarray(ref, dtype=np.float64).reshape(1, 3)
-    positions = grid_positions(dims)
     if vertices is not None:
-        positions = positions[np.asarray(vertices)]
+        positions = grid_positions_of(dims, vertices)
+    else:
+        positions = grid_positions(dims)
     ref_is_mu = role == "reference-is-mu"
     ref_grid = model.grid_mu if ref_is_mu else model.grid_nu
     query_grid = model.grid_nu if ref_is_mu else model.grid_mu
@@ -455,9 +470,10 @@ def ground_truth_field(grids, measure, ref, dims, k=3, chunk=4096, vertices=None
     ``grids`` is (N, nz, ny, nx) fp32.  ``vertices`` optionally restricts the
     evaluation to a subset of flat grid indices (bounded CPU samples).
     """
-    positions = grid_positions(dims)
     if vertices is not None:
-        positions = positions[np.asarray(vertices)]
+        positions = grid_positions_of(dims, vertices)
+    else:
+        positions = grid_positions(dims)
     ref = np.asarray(ref, dtype=np.float64).reshape(3)
     ref_vec = sample_many(grids, ref.reshape(1, 3))[0]
     if measure == "pearson":

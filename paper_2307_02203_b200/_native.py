@@ -23,7 +23,7 @@ NDF_MAX_WIDTH = 256
 MERGE = {"multiply": 0, "concat": 1, "add": 2, "absdiff": 3, "sum_absdiff": 4}
 ACT = {"relu": 0, "snake": 1, "snake_alt": 2, "silu": 3}
 HEAD = {"linear": 0, "tanh": 1, "softplus": 2}
-PREC = {"fp32": 0, "bf16": 1}
+PREC = {"fp32": 0, "bf16": 1, "fp16": 2}
 
 _c_p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -43,6 +43,7 @@ class ModelDesc(ctypes.Structure):
         ("head", _i32),
         ("n_layers", _i32),
         ("widths", _i32 * (NDF_MAX_LAYERS + 1)),
+        ("tc_format", _i32),
         ("grid_mu", _c_p),
         ("grid_nu", _c_p),
         ("params_f32", _c_p),

@@ -16,6 +16,7 @@ struct QueryArgs {
   int64_t n_mu;
   const double* p_nu;
   float* out;
+  int prec;                 // NDF_PREC_*
 };
 
 // flat vertex (x fastest) -> node coordinates (measures.py:240-252)

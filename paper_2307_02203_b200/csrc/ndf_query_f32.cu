@@ -203,7 +203,9 @@ extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, dou
   a.nx = nx; a.ny = ny; a.nz = nz;
   a.v0 = v0; a.v1 = v1;
   a.out = out;
-  if (precision == NDF_PREC_BF16) return launch_query_tc(a, as_stream(stream));
+  a.prec = precision;
+  if (precision == NDF_PREC_BF16 || precision == NDF_PREC_FP16)
+    return launch_query_tc(a, as_stream(stream));
   NDF_REQUIRE(precision == NDF_PREC_FP32, NDF_ERR_PARAMETER, "unknown precision");
   return launch_query_f32(a, as_stream(stream));
 }
@@ -225,7 +227,9 @@ extern "C" int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int
   a.v0 = 0; a.v1 = n;
   a.p_mu = p_mu; a.n_mu = n_mu; a.p_nu = p_nu;
   a.out = out;
-  if (precision == NDF_PREC_BF16) return launch_query_tc(a, as_stream(stream));
+  a.prec = precision;
+  if (precision == NDF_PREC_BF16 || precision == NDF_PREC_FP16)
+    return launch_query_tc(a, as_stream(stream));
   NDF_REQUIRE(precision == NDF_PREC_FP32, NDF_ERR_PARAMETER, "unknown precision");
   return launch_query_f32(a, as_stream(stream));
 }

@@ -145,9 +145,15 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
+template <bool F16>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (F16) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
@@ -191,7 +197,7 @@ __device__ __forceinline__ float merged_value(int merge, int idx, FA ea, FB eb) 
 }
 
 // Write one row of the layer-0 A operand (bf16, canonical layout).
-template <class FA, class FB>
+template <bool F16, class FA, class FB>
 __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int merge, FA ea, FB eb,
                                                 int kin) {
 #pragma unroll
@@ -200,12 +206,13 @@ __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int mer
       float x[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] = merged_value(merge, 8 * kg + j, ea, eb);
-      st_shared_v4(abase + canon_off(row, kg * 8, kSboA), pack_bf16(x[0], x[1]),
-                   pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+      st_shared_v4(abase + canon_off(row, kg * 8, kSboA), pack2<F16>(x[0], x[1]),
+                   pack2<F16>(x[2], x[3]), pack2<F16>(x[4], x[5]), pack2<F16>(x[6], x[7]));
     }
   }
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(512, 1)
 query_tc_kernel(const QueryArgs a, const int nwg) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -254,9 +261,11 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
   const uint32_t a_addr = smem_u32(abuf);
   const uint32_t w_addr = smem_u32(wblob);
   uint64_t* bar = &bars[1 + wg];
-  // kind::f16 instruction descriptor: D fp32, A/B bf16, K-major both, N=128, M=128
-  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kHid >> 3) << 17) |
-                         ((uint32_t)(kTileM >> 4) << 24);
+  // kind::f16 instruction descriptor: D fp32, A/B bf16 (1) or fp16 (0), K-major both,
+  // N = 128 (bits 17-22, N>>3), M = 128 (bits 24-28, M>>4)
+  const uint32_t ab_fmt = F16 ? 0u : 1u;
+  const uint32_t idesc = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
+                         ((uint32_t)(kHid >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
   const int sbo_w0 = (lay.kin / 8) * 128;
 
   mbar_wait(&bars[0], 0);    // parameters resident
@@ -281,8 +290,8 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
         embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, grid_q, p[0], p[1], p[2], eq);
         auto fq = [&](int i) { return eq[i]; };
         auto fr = [&](int i) { return e_ref[i]; };
-        if (a.ref_is_mu) write_input_row(a_addr, wtid, a.m.merge, fr, fq, lay.kin);
-        else write_input_row(a_addr, wtid, a.m.merge, fq, fr, lay.kin);
+        if (a.ref_is_mu) write_input_row<F16>(a_addr, wtid, a.m.merge, fr, fq, lay.kin);
+        else write_input_row<F16>(a_addr, wtid, a.m.merge, fq, fr, lay.kin);
       } else {
         float em[kE];
         const int64_t im = a.n_mu == 1 ? 0 : gv;
@@ -292,11 +301,11 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
                               a.p_nu[3 * gv + 1], a.p_nu[3 * gv + 2], eq);
         auto fm = [&](int i) { return em[i]; };
         auto fq = [&](int i) { return eq[i]; };
-        write_input_row(a_addr, wtid, a.m.merge, fm, fq, lay.kin);
+        write_input_row<F16>(a_addr, wtid, a.m.merge, fm, fq, lay.kin);
       }
     } else {
       auto fz = [](int) { return 0.0f; };
-      write_input_row(a_addr, wtid, NDF_MERGE_ADD, fz, fz, lay.kin);
+      write_input_row<F16>(a_addr, wtid, NDF_MERGE_ADD, fz, fz, lay.kin);
     }
     fence_proxy_async();
     tc_fence_before();
@@ -334,9 +343,9 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA), pack_bf16(v[8 * j], v[8 * j + 1]),
-                         pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
-                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA),
+                         pack2<F16>(v[8 * j], v[8 * j + 1]), pack2<F16>(v[8 * j + 2], v[8 * j + 3]),
+                         pack2<F16>(v[8 * j + 4], v[8 * j + 5]), pack2<F16>(v[8 * j + 6], v[8 * j + 7]));
         }
       }
       if (!last) fence_proxy_async();
@@ -383,7 +392,10 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
       uint8_t* dst = blob + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
       for (int64_t e = gtid; e < (int64_t)K * N; e += gsz) {
         const int k = (int)(e / N), nn = (int)(e % N);
-        *reinterpret_cast<__nv_bfloat16*>(dst + canon_off(nn, k, sbo)) = __float2bfloat16_rn(W[e]);
+        if (m.tc_format == NDF_PREC_FP16)
+          *reinterpret_cast<__half*>(dst + canon_off(nn, k, sbo)) = __float2half_rn(W[e]);
+        else
+          *reinterpret_cast<__nv_bfloat16*>(dst + canon_off(nn, k, sbo)) = __float2bfloat16_rn(W[e]);
       }
       for (int64_t e = gtid; e < N; e += gsz) vecs[l * kHid + e] = b[e];
     } else {
@@ -415,7 +427,9 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) {
   std::string why;
   NDF_REQUIRE(tc_supported(a.m, &why), NDF_ERR_UNSUPPORTED, why);
   NDF_REQUIRE(a.m.params_tc != nullptr, NDF_ERR_PARAMETER,
-              "bf16 query needs the packed tensor-core blob (ndf_tc_pack)");
+              "tensor-core query needs the packed parameter blob (ndf_tc_pack)");
+  NDF_REQUIRE(a.m.tc_format == a.prec, NDF_ERR_PARAMETER,
+              "packed blob element type does not match the requested precision");
   const tc::Layout lay = tc::make_layout(a.m);
   const int blob_al = (lay.blob_bytes + 1023) & ~1023;
   int nwg = (tc::kMaxSmem - blob_al - 1024) / tc::kABytes;
@@ -423,14 +437,20 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)blob_al + (size_t)nwg * tc::kABytes + 1024;
   static size_t attr_smem = 0;
   if (attr_smem < smem) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel,
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_smem = smem;
   }
   const int64_t n = a.v1 - a.v0;
   const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
   const int64_t ctas = std::min<int64_t>((tiles + nwg - 1) / nwg, sm_count());
-  tc::query_tc_kernel<<<(unsigned)std::max<int64_t>(ctas, 1), nwg * 128, smem, s>>>(a, nwg);
+  const unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
+  if (a.prec == NDF_PREC_FP16)
+    tc::query_tc_kernel<true><<<grid, nwg * 128, smem, s>>>(a, nwg);
+  else
+    tc::query_tc_kernel<false><<<grid, nwg * 128, smem, s>>>(a, nwg);
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }
@@ -453,6 +473,8 @@ extern "C" int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_byte
   NDF_REQUIRE((reinterpret_cast<uintptr_t>(blob) & 15) == 0, NDF_ERR_PARAMETER,
               "blob must be 16-byte aligned");
   NDF_REQUIRE(m->params_f32 != nullptr, NDF_ERR_PARAMETER, "null params_f32");
+  NDF_REQUIRE(m->tc_format == NDF_PREC_BF16 || m->tc_format == NDF_PREC_FP16, NDF_ERR_PARAMETER,
+              "tc_format must be NDF_PREC_BF16 or NDF_PREC_FP16");
   tc::pack_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
   NDF_LAUNCH_CHECK();
   tc::pack_fill_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);

@@ -137,8 +137,10 @@ def pearson_against(ref, samples) -> np.ndarray:
     B, M = samples.shape
     out = torch.empty(B, dtype=torch.float64, device=dev)
     if B:
-        N.call("ndf_pearson_rows", N.ptr(_to_dev_f64(ref, dev)), 0, N.ptr(_to_dev_f64(samples, dev)),
-               M, B, N.ptr(out), N.stream_handle(dev))
+        # keep the device copies referenced until the kernel is enqueued
+        dref, dsmp = _to_dev_f64(ref, dev), _to_dev_f64(samples, dev)
+        N.call("ndf_pearson_rows", N.ptr(dref), 0, N.ptr(dsmp), M, B, N.ptr(out),
+               N.stream_handle(dev))
     return out.cpu().numpy()
 
 
@@ -153,8 +155,8 @@ def pearson_rowwise(a, b) -> np.ndarray:
     B, M = a.shape
     out = torch.empty(B, dtype=torch.float64, device=dev)
     if B:
-        N.call("ndf_pearson_rows", N.ptr(_to_dev_f64(a, dev)), M, N.ptr(_to_dev_f64(b, dev)), M, B,
-               N.ptr(out), N.stream_handle(dev))
+        da, db = _to_dev_f64(a, dev), _to_dev_f64(b, dev)
+        N.call("ndf_pearson_rows", N.ptr(da), M, N.ptr(db), M, B, N.ptr(out), N.stream_handle(dev))
     return out.cpu().numpy()
 
 
@@ -191,7 +193,8 @@ def ksg_rows(a, b, k: int, return_counts: bool = False):
     mi = torch.empty(B, dtype=torch.float64, device=dev)
     counts = torch.empty((B, 2, M), dtype=torch.int32, device=dev) if return_counts else None
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    N.call("ndf_ksg_rows", N.ptr(_to_dev_f64(a, dev)), a_stride, N.ptr(_to_dev_f64(b, dev)), M, B, k,
+    da, db = _to_dev_f64(a, dev), _to_dev_f64(b, dev)
+    N.call("ndf_ksg_rows", N.ptr(da), a_stride, N.ptr(db), M, B, k,
            N.ptr(jit), N.ptr(psi), _KsgTables.psi_km(k, M), N.ptr(mi), None, N.ptr(counts),
            N.ptr(status), N.stream_handle(dev))
     if int(status.item()):

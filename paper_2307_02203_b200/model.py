@@ -30,7 +30,7 @@ NDFM_VERSION = 1
 MERGE_MODES = ("multiply", "concat", "add", "absdiff", "sum_absdiff")
 ACTIVATIONS = ("relu", "snake", "snake_alt", "silu")
 HEADS = ("linear", "tanh", "softplus")
-PRECISIONS = ("fp32", "bf16")
+PRECISIONS = ("fp32", "bf16", "fp16")
 
 
 @dataclass(frozen=True)
@@ -51,7 +51,7 @@ class ModelSpec:
     encoder_layers: int = 0
     decoder_layers: int = 4
     channels: int = 128
-    # --- BASELINE extensions ---
+    # --- BASELINE extensions (precision: "fp32" exact SIMT, "bf16"/"fp16" tcgen05) ---
     grid_resolution: tuple | None = None     # dense latent (rx, ry, rz); None = isotropic level 0
     activation: str = "silu"
     head: str | None = None                  # None: tanh for pearson, softplus for ksg_mi
@@ -294,6 +294,7 @@ class DeviceModel:
         d.grid_nu = self.grid_nu.data_ptr()
         d.params_f32 = self.params.data_ptr()
         d.params_tc = None
+        d.tc_format = N.PREC["fp16"] if spec.precision == "fp16" else N.PREC["bf16"]
         self.blob = None
         lib = N.load_library()
         nbytes = int(lib.ndf_tc_blob_bytes(ctypes_ref(d)))
@@ -301,7 +302,7 @@ class DeviceModel:
             self.blob = torch.empty(nbytes, dtype=torch.uint8, device=device)
             N.call("ndf_tc_pack", ctypes_ref(d), N.ptr(self.blob), nbytes, N.stream_handle(device))
             d.params_tc = self.blob.data_ptr()
-        elif spec.precision == "bf16":
+        elif spec.precision in ("bf16", "fp16"):
             raise ConfigError("model is outside the tcgen05 kernel envelope (L=6, C=16, "
                               "hidden width 128, input width <= 128); use precision='fp32'")
         self.desc = d

@@ -74,7 +74,17 @@ def reconstruct_field(model: NdfModel, ref, role: str = ROLE_MU, dims=(64, 64, 6
         raise ParameterError("batch_size must be >= 1")
     dims = _check_dims(dims)
     out = reconstruct_field_device(model, ref, role, dims, clamp=clamp)
-    return FieldGrid(dims, out.cpu().numpy())
+    return FieldGrid(dims, to_host(out))
+
+
+def to_host(t) -> np.ndarray:
+    """D2H through pinned memory (torch's caching host allocator): one async copy,
+    one stream sync; the returned array owns the pinned block until freed."""
+    import torch
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return host.numpy()
 
 
 def difference_field(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,
