@@ -68,16 +68,28 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        """Start sampling and block until the first sample arrived (so the whole
+        timed region that follows is bracketed by samples)."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
+
+    def stop(self):
+        """Wait for one more sample after the timed region, then stop."""
+        n = len(self.samples)
+        t0 = time.time()
+        while self.proc is not None and len(self.samples) <= n and time.time() - t0 < 2:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -86,6 +98,7 @@ class ClockSampler:
                 self.samples.append(parts)
 
     def __exit__(self, *exc):
+        self.stop()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -440,8 +453,8 @@ def main():
     ap.add_argument("--precision", choices=["fp16", "bf16", "fp32"], default="fp16")
     ap.add_argument("--quick", action="store_true", help="query only (profiling runs)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 16)
-    ap.add_argument("--cpu-ksg-pairs", type=int, default=256)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 19)
+    ap.add_argument("--cpu-ksg-pairs", type=int, default=2048)
     ap.add_argument("--ksg-pairs", type=int, default=1 << 15)
     ap.add_argument("--ref-sample", type=int, default=1 << 14)
     args = ap.parse_args()

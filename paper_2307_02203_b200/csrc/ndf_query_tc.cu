@@ -2,12 +2,13 @@
 //
 //   embed (fp64 -> fp32, bit-exact with model.py:169-177)
 //   -> merge [e_r + e_q, |e_r - e_q|]                      (model.py:279-286 + BASELINE)
-//   -> H x { tcgen05.mma bf16 x bf16 -> fp32 (TMEM) ; bias + activation in the
-//            tcgen05.ld epilogue ; bf16 back to SMEM as the next A operand }
-//   -> output layer (128 -> 1) as an fp32 dot product in the last epilogue -> head.
+//   -> H x { tcgen05.mma 16-bit x 16-bit -> fp32 accumulator in TMEM ;
+//            tcgen05.ld epilogue: bias + activation, packed back to SMEM as the
+//            next layer's A operand }
+//   -> output layer 128 -> 1 as a 16-column tcgen05.mma (zero-padded B) -> head.
 //
 // Layout / schedule (one persistent CTA per SM, NWG <= 4 warpgroups):
-//   * the packed parameter blob (UMMA-canonical K-major bf16 weights + fp32 bias
+//   * the packed parameter blob (UMMA-canonical K-major 16-bit weights + fp32 bias
 //     vectors) is fetched once per CTA by the bulk-copy engine (cp.async.bulk ->
 //     mbarrier complete_tx) and stays resident in SMEM;
 //   * each warpgroup owns a 128-row tile of query vertices, one 32 KB A buffer
@@ -16,14 +17,25 @@
 //     (row m of the tile = TMEM lane m = thread m of the warpgroup);
 //   * one thread per warpgroup issues the K/16 tcgen05.mma steps of a layer and
 //     commits them to the warpgroup's mbarrier; while one warpgroup runs its
-//     epilogue (MUFU/ALU-bound), the other warpgroups' MMAs keep the tensor pipe
-//     busy -- a 4-way ping-pong without any CTA-wide barrier.
+//     epilogue, the other warpgroups' MMAs keep the tensor pipe busy -- a 4-way
+//     ping-pong without any CTA-wide barrier.
+//   * every accumulator is pre-loaded with its layer's bias (tcgen05.st while the
+//     previous layer's values are drained), so the MMAs accumulate onto the bias
+//     and the epilogue has no bias adds;
+//   * SiLU layers are packed with W and b pre-scaled by 1/2 (exact in 16-bit), so
+//     the accumulator holds x/2 and silu(x) = x/2 + (x/2)*tanh(x/2) is one
+//     tanh.approx (MUFU) and one FMA per element, then a paired 16-bit pack.
+//   * grid-mode Fourier features are per-axis: a prep kernel evaluates them once
+//     per axis node (same fp64 sincos, so the same bits) and the query reads them.
+//   * multi-reference queries (BASELINE config 3) embed each query vertex once and
+//     reuse it for every reference (refs' embeddings come from the prep kernel).
 #include <algorithm>
+#include <string>
 
 #include "ndf_query.cuh"
+#include "ndf_tc_ptx.cuh"
 
 namespace ndf {
-
 namespace tc {
 
 constexpr int kHid = 128;           // hidden width (UMMA N)
@@ -33,14 +45,17 @@ constexpr int kSboA = (kHid / 8) * 128;        // 2048 B between 8-row groups
 constexpr int kL = 6;               // Fourier octaves supported by the fused encoder
 constexpr int kC = 16;              // latent channels supported by the fused encoder
 constexpr int kE = 3 + 6 * kL + kC; // 55
+constexpr int kERefStride = 64;     // floats per prepared reference embedding
+constexpr int kOutN = 16;           // output-layer MMA width (column 0 is the result)
 constexpr int kMaxSmem = 232448;    // 227 KB opt-in
 
 struct Layout {
-  int H;            // MMA layers (hidden layers)
+  int H;            // hidden layers (MMA stages before the output stage)
   int kin;          // padded layer-0 K (multiple of 16, <= 128)
-  int w0_bytes;     // 128 x kin bf16
-  int wh_bytes;     // 128 x 128 bf16
-  int vec_off;      // byte offset of fp32 vectors (biases, w_out, b_out)
+  int w0_bytes;     // 128 x kin
+  int wh_bytes;     // 128 x 128
+  int wout_off;     // 16 x 128 output-layer B operand
+  int vec_off;      // fp32: bias[H][128], b_out, pad
   int blob_bytes;   // multiple of 16
 };
 
@@ -50,9 +65,9 @@ __host__ __device__ inline Layout make_layout(const ndf_model_desc& m) {
   L.kin = (m.widths[0] + 15) / 16 * 16;
   L.w0_bytes = kHid * L.kin * 2;
   L.wh_bytes = kHid * kHid * 2;
-  L.vec_off = L.w0_bytes + (L.H - 1) * L.wh_bytes;
-  const int vec_bytes = (L.H * kHid + kHid + 4) * 4;
-  L.blob_bytes = L.vec_off + vec_bytes;
+  L.wout_off = L.w0_bytes + (L.H - 1) * L.wh_bytes;
+  L.vec_off = L.wout_off + kOutN * kHid * 2;
+  L.blob_bytes = L.vec_off + (L.H * kHid + 4) * 4;
   return L;
 }
 
@@ -61,124 +76,50 @@ __host__ __device__ __forceinline__ int canon_off(int r, int k, int sbo) {
   return (r >> 3) * sbo + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
 }
 
-// ---------------------------------------------------------------------------
-// PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+      "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+      "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+      "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
-  d |= (uint64_t)(lbo >> 4) << 16;
-  d |= (uint64_t)(sbo >> 4) << 32;
-  d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
-  return d;                           // base_offset 0, lbo_mode 0, SWIZZLE_NONE
-}
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-template <bool F16>
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  if constexpr (F16) {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  } else {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                             uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d)
-               : "memory");
 }
 
-// Hidden activation for the bf16 path (fast forms; within the 1e-2 bf16 contract).
-__device__ __forceinline__ float act_fast(int kind, float x) {
-  switch (kind) {
-    case NDF_ACT_SILU: {            // x*sigmoid(x) = hx + hx*tanh(hx), hx = x/2 (1 MUFU op)
-      const float hx = 0.5f * x;
-      return fmaf(hx, tanh_fast(hx), hx);
+// Write layer-0's bias (fp32, pre-scaled for SiLU) into this thread's accumulator row.
+__device__ __forceinline__ void preload_bias(uint32_t tmem_row, const float* bias) {
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
+#pragma unroll 1
+  for (int c0 = 0; c0 < kHid; c0 += 32) {
+    uint32_t nb[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = b4[(c0 >> 2) + q];
+      nb[4 * q] = __float_as_uint(b.x); nb[4 * q + 1] = __float_as_uint(b.y);
+      nb[4 * q + 2] = __float_as_uint(b.z); nb[4 * q + 3] = __float_as_uint(b.w);
     }
+    tmem_st32(tmem_row + (uint32_t)c0, nb);
+  }
+}
+
+// Generic (non-SiLU) hidden activations, fp32 fast forms (nn.py:23-32).
+__device__ __forceinline__ float act_f32(int kind, float x) {
+  switch (kind) {
     case NDF_ACT_RELU: return fmaxf(x, 0.0f);
     case NDF_ACT_SNAKE: { const float s = __sinf(x); return fmaf(s, s, x); }
-    default: return 0.5f * (x + 1.0f - __cosf(2.0f * x));
+    case NDF_ACT_SNAKE_ALT: return 0.5f * (x + 1.0f - __cosf(2.0f * x));
+    default: { const float hx = 0.5f * x; return fmaf(hx, tanh_fast(hx), hx); }
   }
 }
 
-// Merged decoder-input element idx (model.py:279-286 + BASELINE's sum_absdiff),
-// computed in fp32 from the two embeddings (ea = mu branch, eb = nu branch).
-template <class FA, class FB>
-__device__ __forceinline__ float merged_value(int merge, int idx, FA ea, FB eb) {
+// Merged decoder-input element idx (model.py:279-286 + BASELINE's sum_absdiff).
+// MERGE >= 0 fixes the mode at compile time; -1 reads it at run time.
+template <int MERGE, class FA, class FB>
+__device__ __forceinline__ float merged_value(int merge_rt, int idx, FA ea, FB eb) {
+  const int merge = MERGE >= 0 ? MERGE : merge_rt;
   if (idx < kE) {
     const float a = ea(idx), b = eb(idx);
     switch (merge) {
@@ -196,8 +137,7 @@ __device__ __forceinline__ float merged_value(int merge, int idx, FA ea, FB eb) 
   return 0.0f;
 }
 
-// Write one row of the layer-0 A operand (bf16, canonical layout).
-template <bool F16, class FA, class FB>
+template <bool F16, int MERGE, class FA, class FB>
 __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int merge, FA ea, FB eb,
                                                 int kin) {
 #pragma unroll
@@ -205,22 +145,139 @@ __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int mer
     if (kg * 8 < kin) {
       float x[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = merged_value(merge, 8 * kg + j, ea, eb);
+      for (int j = 0; j < 8; ++j) x[j] = merged_value<MERGE>(merge, 8 * kg + j, ea, eb);
       st_shared_v4(abase + canon_off(row, kg * 8, kSboA), pack2<F16>(x[0], x[1]),
                    pack2<F16>(x[2], x[3]), pack2<F16>(x[4], x[5]), pack2<F16>(x[6], x[7]));
     }
   }
 }
 
-template <bool F16>
+// Latent-grid trilinear lookup in fp32 (the 16-bit path rounds every merged input
+// to 11/8 significant bits, so fp32 corner sums are exact enough by 2^-13 and keep
+// the fp64 and conversion units free).  Same corner order and clamping rules as
+// the reference (encoding.py:105-118).
+__device__ __forceinline__ void latent_f32(const float* __restrict__ grid, int rx, int ry, int rz,
+                                           double px, double py, double pz, float* out) {
+  const AxisCoord cx = level_coord(px, rx);
+  const AxisCoord cy = level_coord(py, ry);
+  const AxisCoord cz = level_coord(pz, rz);
+  const float tx = (float)cx.t, ty = (float)cy.t, tz = (float)cz.t;
+  float acc[kC];
+#pragma unroll
+  for (int ch = 0; ch < kC; ++ch) acc[ch] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+    const float w = (dx ? tx : 1.0f - tx) * (dy ? ty : 1.0f - ty) * (dz ? tz : 1.0f - tz);
+    const int idx = (cx.i0 + dx) + rx * ((cy.i0 + dy) + ry * (cz.i0 + dz));
+    const float4* row = reinterpret_cast<const float4*>(grid + (size_t)idx * kC);
+#pragma unroll
+    for (int q = 0; q < kC / 4; ++q) {
+      const float4 f = __ldg(row + q);
+      acc[4 * q + 0] = fmaf(w, f.x, acc[4 * q + 0]);
+      acc[4 * q + 1] = fmaf(w, f.y, acc[4 * q + 1]);
+      acc[4 * q + 2] = fmaf(w, f.z, acc[4 * q + 2]);
+      acc[4 * q + 3] = fmaf(w, f.w, acc[4 * q + 3]);
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < kC; ++ch) out[ch] = acc[ch];
+}
+
+// Grid-mode embedding of node (ix, iy, iz): raw coords, the per-axis Fourier block
+// from the table written by prep_kernel (fp64 sincos, cast once), the latent part
+// from latent_f32.
+__device__ __forceinline__ void embed_grid_node(const QueryArgs& a, const float* __restrict__ grid,
+                                                const float* __restrict__ ftab, int64_t v,
+                                                float* e) {
+  const int64_t plane = (int64_t)a.nx * a.ny;
+  const int iz = (int)(v / plane);
+  const int64_t r = v - (int64_t)iz * plane;
+  const int iy = (int)(r / a.nx);
+  const int ix = (int)(r - (int64_t)iy * a.nx);
+  const double p[3] = {node_coord(ix, a.nx), node_coord(iy, a.ny), node_coord(iz, a.nz)};
+  e[0] = (float)p[0];
+  e[1] = (float)p[1];
+  e[2] = (float)p[2];
+  const int rows[3] = {ix, a.nx + iy, a.nx + a.ny + iz};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const float4* t = reinterpret_cast<const float4*>(ftab + (size_t)rows[ax] * (2 * kL));
+#pragma unroll
+    for (int q = 0; q < (2 * kL) / 4; ++q) {
+      const float4 f = __ldg(t + q);
+      const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * q + u;            // j = 2*octave + (0 sin | 1 cos)
+        e[3 + 6 * (j >> 1) + 2 * ax + (j & 1)] = fv[u];
+      }
+    }
+  }
+  latent_f32(grid, a.g.rx, a.g.ry, a.g.rz, p[0], p[1], p[2], e + 3 + 6 * kL);
+}
+
+// Points-mode embedding (NdfModel.forward): fp64 sincos per point, fp32 latent.
+__device__ __forceinline__ void embed_point_tc(const QueryArgs& a, const float* __restrict__ grid,
+                                               const double* pos, float* e) {
+  const double p[3] = {fmin(fmax(pos[0], -1.0), 1.0), fmin(fmax(pos[1], -1.0), 1.0),
+                       fmin(fmax(pos[2], -1.0), 1.0)};
+  e[0] = (float)p[0];
+  e[1] = (float)p[1];
+  e[2] = (float)p[2];
+  double scale = 3.141592653589793;
+#pragma unroll
+  for (int i = 0; i < kL; ++i) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double sn, cs;
+      sincos(dmul(scale, p[ax]), &sn, &cs);
+      e[3 + 6 * i + 2 * ax] = (float)sn;
+      e[3 + 6 * i + 2 * ax + 1] = (float)cs;
+    }
+    scale = scale * 2.0;
+  }
+  latent_f32(grid, a.g.rx, a.g.ry, a.g.rz, p[0], p[1], p[2], e + 3 + 6 * kL);
+}
+
+struct TcArgs {
+  QueryArgs q;
+  const float* ftab;      // grid mode: (nx+ny+nz) x 2L Fourier table
+  const float* erefs;     // grid mode: n_ref x kERefStride reference embeddings
+  int n_ref;
+  uint16_t* out16;        // multi-ref output (fp16), rows of ld_out
+  int64_t ld_out;
+};
+
+// One MMA stage: K/16 tcgen05.mma steps into the warpgroup's accumulator, committed
+// to its mbarrier.  Issued by one thread.
+// acc_first = 1: the accumulator was pre-loaded (bias) and every step accumulates.
+__device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr,
+                                            int K, uint32_t sbo_b, uint32_t idesc, uint64_t* bar,
+                                            uint32_t acc_first) {
+  tc_fence_after();
+  for (int kk = 0; kk < K / 16; ++kk) {
+    const uint64_t ad = smem_desc(a_addr + kk * 256, 128, kSboA);
+    const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
+    mma_bf16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : acc_first);
+  }
+  mma_commit(bar);
+}
+
+// F16: fp16 (true) or bf16 operands.  SILU: SiLU-specialised epilogue (packed
+// 16-bit tanh/fma) vs generic fp32 activation.  KIND: 0 = grid, one reference;
+// 1 = grid, several references per query vertex (the query embedding stays live
+// across them); 2 = paired points (NdfModel.forward).
+constexpr int kGridSingle = 0, kGridMulti = 1, kPoints = 2;
+template <bool F16, bool SILU, int KIND>
 __global__ void __launch_bounds__(512, 1)
-query_tc_kernel(const QueryArgs a, const int nwg) {
+query_tc_kernel(const TcArgs t, const int nwg) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const QueryArgs& a = t.q;
   const Layout lay = make_layout(a.m);
   uint8_t* wblob = smem;                                   // parameter blob
   uint8_t* abufs = smem + ((lay.blob_bytes + 1023) & ~1023);
-  float* e_ref = reinterpret_cast<float*>(abufs + nwg * kABytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(e_ref + 64);   // [0] weights, [1+w] per WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + nwg * kABytes);   // [0] weights, [1+w]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int tid = threadIdx.x;
@@ -241,10 +298,6 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
                  "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (a.mode == 0 && tid == 32) {
-    const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
-    embed_point(a.g, grid, a.ref[0], a.ref[1], a.ref[2], [&](int i, float v) { e_ref[i] = v; });
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -257,18 +310,21 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t d_tmem = tmem_base + (uint32_t)(wg * kHid);       // column offset
   const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;    // TMEM lane quarter
-  uint8_t* abuf = abufs + wg * kABytes;
-  const uint32_t a_addr = smem_u32(abuf);
+  const uint32_t a_addr = smem_u32(abufs + wg * kABytes);
+  const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(wg * kHid);  // this thread's lane
   const uint32_t w_addr = smem_u32(wblob);
   uint64_t* bar = &bars[1 + wg];
-  // kind::f16 instruction descriptor: D fp32, A/B bf16 (1) or fp16 (0), K-major both,
-  // N = 128 (bits 17-22, N>>3), M = 128 (bits 24-28, M>>4)
+  // kind::f16 instruction descriptor: D fp32 (bit 4), A/B fp16 (0) or bf16 (1) at bits
+  // 7-9 / 10-12, both K-major, N>>3 at bits 17-22, M>>4 at bits 24-28.
   const uint32_t ab_fmt = F16 ? 0u : 1u;
-  const uint32_t idesc = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
-                         ((uint32_t)(kHid >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-  const int sbo_w0 = (lay.kin / 8) * 128;
+  const uint32_t idesc_base = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
+                              ((uint32_t)(kTileM >> 4) << 24);
+  const uint32_t idesc = idesc_base | ((uint32_t)(kHid >> 3) << 17);
+  const uint32_t idesc_out = idesc_base | ((uint32_t)(kOutN >> 3) << 17);
+  const uint32_t sbo_w0 = (uint32_t)(lay.kin / 8) * 128;
 
   mbar_wait(&bars[0], 0);    // parameters resident
+  const float bias_out = vecs[lay.H * kHid];
 
   const int64_t n = a.v1 - a.v0;
   const int64_t n_tiles = (n + kTileM - 1) / kTileM;
@@ -276,85 +332,115 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
   uint32_t phase = 0;
   const float* grid_q = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
   const int bar_id = 1 + wg;
+  const int n_ref = KIND == kGridMulti ? t.n_ref : 1;
 
   for (int64_t tile = (int64_t)blockIdx.x * nwg + wg; tile < n_tiles; tile += stride) {
     const int64_t vloc = tile * kTileM + wtid;   // local vertex index
     const bool valid = vloc < n;
-    // ---- K1: embed + merge -> A (bf16) ----------------------------------------
-    if (valid) {
-      const int64_t gv = a.v0 + vloc;
-      float eq[kE];
-      if (a.mode == 0) {
-        double p[3];
-        vertex_position(a, gv, p);
-        embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, grid_q, p[0], p[1], p[2], eq);
-        auto fq = [&](int i) { return eq[i]; };
-        auto fr = [&](int i) { return e_ref[i]; };
-        if (a.ref_is_mu) write_input_row<F16>(a_addr, wtid, a.m.merge, fr, fq, lay.kin);
-        else write_input_row<F16>(a_addr, wtid, a.m.merge, fq, fr, lay.kin);
+    // ---- K1: embed the query vertex once -----------------------------------------
+    float eq[kE];
+    if (valid && KIND != kPoints) {
+      embed_grid_node(a, grid_q, t.ftab, a.v0 + vloc, eq);
+    } else if (valid) {
+      embed_point_tc(a, a.m.grid_nu, a.p_nu + 3 * (a.v0 + vloc), eq);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
+    }
+    for (int r = 0; r < n_ref; ++r) {
+      // ---- bias of layer 0 -> accumulator (tcgen05.st); the MMAs then accumulate ----
+      preload_bias(tmem_row, vecs);
+      // ---- merge -> A ------------------------------------------------------------
+      auto fq = [&](int i) { return eq[i]; };
+      if constexpr (KIND != kPoints) {
+        const float* er = t.erefs + (size_t)r * kERefStride;
+        auto fr = [&](int i) { return __ldg(er + i); };
+        if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)      // symmetric: role does not matter
+          write_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(a_addr, wtid, 0, fr, fq, lay.kin);
+        else if (a.ref_is_mu)
+          write_input_row<F16, -1>(a_addr, wtid, a.m.merge, fr, fq, lay.kin);
+        else
+          write_input_row<F16, -1>(a_addr, wtid, a.m.merge, fq, fr, lay.kin);
       } else {
         float em[kE];
-        const int64_t im = a.n_mu == 1 ? 0 : gv;
-        embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, a.m.grid_mu, a.p_mu[3 * im],
-                              a.p_mu[3 * im + 1], a.p_mu[3 * im + 2], em);
-        embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, a.m.grid_nu, a.p_nu[3 * gv],
-                              a.p_nu[3 * gv + 1], a.p_nu[3 * gv + 2], eq);
-        auto fm = [&](int i) { return em[i]; };
-        auto fq = [&](int i) { return eq[i]; };
-        write_input_row<F16>(a_addr, wtid, a.m.merge, fm, fq, lay.kin);
-      }
-    } else {
-      auto fz = [](int) { return 0.0f; };
-      write_input_row<F16>(a_addr, wtid, NDF_MERGE_ADD, fz, fz, lay.kin);
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    named_bar(bar_id, 128);
-    // ---- K2: H tensor-core layers -----------------------------------------------
-    float out_acc = 0.0f;
-    for (int l = 0; l < lay.H; ++l) {
-      if (wtid == 0) {
-        tc_fence_after();
-        const int K = l == 0 ? lay.kin : kHid;
-        const uint32_t wl = w_addr + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
-        const uint32_t sbo_b = l == 0 ? sbo_w0 : kSboA;
-        for (int kk = 0; kk < K / 16; ++kk) {
-          const uint64_t ad = smem_desc(a_addr + kk * 256, 128, kSboA);
-          const uint64_t bd = smem_desc(wl + kk * 256, 128, sbo_b);
-          mma_bf16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+        if (valid) {
+          const int64_t im = a.n_mu == 1 ? 0 : a.v0 + vloc;
+          embed_point_tc(a, a.m.grid_mu, a.p_mu + 3 * im, em);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kE; ++i) em[i] = 0.0f;
         }
-        mma_commit(bar);
+        auto fm = [&](int i) { return em[i]; };
+        write_input_row<F16, -1>(a_addr, wtid, a.m.merge, fm, fq, lay.kin);
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_proxy_async();
+      tc_fence_before();
+      named_bar(bar_id, 128);
+      // ---- K2: hidden layers on the tensor cores --------------------------------------
+      for (int l = 0; l < lay.H; ++l) {
+        if (wtid == 0) {
+          const uint32_t wl = w_addr + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
+          issue_stage(d_tmem, a_addr, wl, l == 0 ? lay.kin : kHid, l == 0 ? sbo_w0 : kSboA,
+                      idesc, bar, 1u);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        const bool next_hidden = l + 1 < lay.H;
+        const float4* nbias4 = reinterpret_cast<const float4*>(vecs + (l + 1) * kHid);
+#pragma unroll 1
+        for (int c0 = 0; c0 < kHid; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem_row + (uint32_t)c0, v);          // z (or z/2 for SiLU) incl. bias
+          if (next_hidden) {                               // next layer's bias -> same columns
+            uint32_t nb[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 b4 = nbias4[(c0 >> 2) + q];
+              nb[4 * q] = __float_as_uint(b4.x); nb[4 * q + 1] = __float_as_uint(b4.y);
+              nb[4 * q + 2] = __float_as_uint(b4.z); nb[4 * q + 3] = __float_as_uint(b4.w);
+            }
+            tmem_st32(tmem_row + (uint32_t)c0, nb);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t p[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x0 = v[8 * j + 2 * q], x1 = v[8 * j + 2 * q + 1];
+              if constexpr (SILU)   // x = z/2: silu(z) = x + x*tanh(x)
+                p[q] = pack2<F16>(fmaf(x0, tanh_fast(x0), x0), fmaf(x1, tanh_fast(x1), x1));
+              else
+                p[q] = pack2<F16>(act_f32(a.m.activation, x0), act_f32(a.m.activation, x1));
+            }
+            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA), p[0], p[1], p[2], p[3]);
+          }
+        }
+        if (next_hidden) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_proxy_async();
+        tc_fence_before();
+        named_bar(bar_id, 128);
+      }
+      // ---- output layer (128 -> 1) as a 16-column MMA ---------------------------------
+      if (wtid == 0)
+        issue_stage(d_tmem, a_addr, w_addr + lay.wout_off, kHid, kSboA, idesc_out, bar, 0u);
       mbar_wait(bar, phase);
       phase ^= 1;
       tc_fence_after();
-      const float* bias = vecs + l * kHid;
-      const bool last = (l == lay.H - 1);
-#pragma unroll 1
-      for (int c0 = 0; c0 < kHid; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + lane_base + (uint32_t)(wg * kHid + c0), v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = act_fast(a.m.activation, v[i] + bias[c0 + i]);
-        if (last) {
-          const float* wo = vecs + lay.H * kHid;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) out_acc = fmaf(v[i], wo[c0 + i], out_acc);
+      uint32_t zr;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                   : "=r"(zr) : "r"(tmem_row));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (valid) {
+        const float z = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
+        if (t.out16) {
+          const __half hz = __float2half_rn(z);
+          t.out16[(size_t)r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&hz);
         } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA),
-                         pack2<F16>(v[8 * j], v[8 * j + 1]), pack2<F16>(v[8 * j + 2], v[8 * j + 3]),
-                         pack2<F16>(v[8 * j + 4], v[8 * j + 5]), pack2<F16>(v[8 * j + 6], v[8 * j + 7]));
+          a.out[vloc] = z;
         }
       }
-      if (!last) fence_proxy_async();
-      tc_fence_before();
-      named_bar(bar_id, 128);
-    }
-    if (valid) {
-      const float z = out_acc + vecs[lay.H * kHid + kHid];
-      a.out[vloc] = head_exact(a.m.head, z);
     }
   }
   tc_fence_before();
@@ -365,19 +451,55 @@ query_tc_kernel(const QueryArgs a, const int nwg) {
                  "r"(tmem_cols));
 }
 
+// ---- per-query prep: per-axis Fourier table + reference embeddings ------------
+__global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, float* ftab,
+                            float* erefs) {
+  const int naxis = a.nx + a.ny + a.nz;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid < naxis) {
+    int ax, i, n;
+    if (tid < a.nx) { ax = 0; i = tid; n = a.nx; }
+    else if (tid < a.nx + a.ny) { ax = 1; i = tid - a.nx; n = a.ny; }
+    else { ax = 2; i = tid - a.nx - a.ny; n = a.nz; }
+    (void)ax;
+    const double p = fmin(fmax(node_coord(i, n), -1.0), 1.0);
+    double scale = 3.141592653589793;
+    for (int o = 0; o < kL; ++o) {
+      double s, c;
+      sincos(dmul(scale, p), &s, &c);
+      ftab[tid * 2 * kL + 2 * o] = (float)s;
+      ftab[tid * 2 * kL + 2 * o + 1] = (float)c;
+      scale = scale * 2.0;
+    }
+  } else if (tid < naxis + n_ref) {
+    const int r = tid - naxis;
+    const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
+    float e[kE];
+    embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, grid, refs[3 * r], refs[3 * r + 1],
+                          refs[3 * r + 2], e);
+    for (int i = 0; i < kERefStride; ++i) erefs[(size_t)r * kERefStride + i] = i < kE ? e[i] : 0.f;
+  }
+}
+
 // ---- parameter packing (device) ---------------------------------------------
-__global__ void pack_kernel(const ndf_model_desc m, uint8_t* blob) {
+__global__ void pack_zero_kernel(const ndf_model_desc m, uint8_t* blob) {
   const Layout lay = make_layout(m);
   const int64_t total = (int64_t)lay.blob_bytes / 4;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
        w += (int64_t)gridDim.x * blockDim.x)
     reinterpret_cast<uint32_t*>(blob)[w] = 0u;
-  __syncthreads();   // per-block only; a grid-wide order is provided by two launches
+}
+
+__device__ __forceinline__ void store16(uint8_t* p, float v, bool f16) {
+  if (f16) *reinterpret_cast<__half*>(p) = __float2half_rn(v);
+  else *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
 }
 
 __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
   const Layout lay = make_layout(m);
-  // weights: layer l (K x N fp32 row-major, N = 128) -> canonical N x Kpad bf16
+  const bool f16 = m.tc_format == NDF_PREC_FP16;
+  // SiLU layers are stored pre-scaled by 1/2 (exact): the accumulator holds x/2.
+  const float hs = m.activation == NDF_ACT_SILU ? 0.5f : 1.0f;
   size_t off = 0;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
@@ -387,20 +509,20 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
     const float* W = m.params_f32 + off;
     const float* b = W + (size_t)K * N;
     if (l < lay.H) {
+      // layer l (K x N fp32 row-major, N = 128) -> canonical N x Kpad, K-major
       const int kpad = l == 0 ? lay.kin : kHid;
       const int sbo = (kpad / 8) * 128;
       uint8_t* dst = blob + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
       for (int64_t e = gtid; e < (int64_t)K * N; e += gsz) {
         const int k = (int)(e / N), nn = (int)(e % N);
-        if (m.tc_format == NDF_PREC_FP16)
-          *reinterpret_cast<__half*>(dst + canon_off(nn, k, sbo)) = __float2half_rn(W[e]);
-        else
-          *reinterpret_cast<__nv_bfloat16*>(dst + canon_off(nn, k, sbo)) = __float2bfloat16_rn(W[e]);
+        store16(dst + canon_off(nn, k, sbo), hs * W[e], f16);
       }
-      for (int64_t e = gtid; e < N; e += gsz) vecs[l * kHid + e] = b[e];
+      for (int64_t e = gtid; e < N; e += gsz) vecs[l * kHid + e] = hs * b[e];
     } else {
-      for (int64_t e = gtid; e < K; e += gsz) vecs[lay.H * kHid + e] = W[e];
-      if (gtid == 0) vecs[lay.H * kHid + kHid] = b[0];
+      // output layer (128 x 1) -> row 0 of a 16 x 128 canonical B operand
+      for (int64_t e = gtid; e < K; e += gsz)
+        store16(blob + lay.wout_off + canon_off(0, (int)e, kSboA), W[e], f16);
+      if (gtid == 0) vecs[lay.H * kHid] = b[0];
     }
     off += (size_t)K * N + N;
   }
@@ -423,7 +545,39 @@ static bool tc_supported(const ndf_model_desc& m, std::string* why) {
   return true;
 }
 
-int launch_query_tc(const QueryArgs& a, cudaStream_t s) {
+template <bool F16, bool SILU, int KIND>
+static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, cudaStream_t s) {
+  static size_t attr = 0;
+  if (attr < smem) {
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<F16, SILU, KIND>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+template <bool F16>
+static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid,
+                             cudaStream_t s) {
+  using namespace tc;
+  const bool silu = t.q.m.activation == NDF_ACT_SILU;
+  const int kind = t.q.mode == 1 ? kPoints : (t.n_ref > 1 ? kGridMulti : kGridSingle);
+  if (silu) {
+    if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, s);
+    if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, s);
+    return launch_tc_t<F16, true, kPoints>(t, nwg, smem, grid, s);
+  }
+  if (kind == kGridSingle) return launch_tc_t<F16, false, kGridSingle>(t, nwg, smem, grid, s);
+  if (kind == kGridMulti) return launch_tc_t<F16, false, kGridMulti>(t, nwg, smem, grid, s);
+  return launch_tc_t<F16, false, kPoints>(t, nwg, smem, grid, s);
+}
+
+// Grid / points query on the tensor cores; refs (device, n_ref x 3) and out16 are
+// only used by the multi-reference entry point.
+static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_t* out16,
+                  int64_t ld_out, cudaStream_t s) {
   std::string why;
   NDF_REQUIRE(tc_supported(a.m, &why), NDF_ERR_UNSUPPORTED, why);
   NDF_REQUIRE(a.m.params_tc != nullptr, NDF_ERR_PARAMETER,
@@ -432,28 +586,47 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) {
               "packed blob element type does not match the requested precision");
   const tc::Layout lay = tc::make_layout(a.m);
   const int blob_al = (lay.blob_bytes + 1023) & ~1023;
-  int nwg = (tc::kMaxSmem - blob_al - 1024) / tc::kABytes;
-  nwg = std::min(nwg, 4);
+  const int nwg = std::min((tc::kMaxSmem - blob_al - 1024) / tc::kABytes, 4);
   const size_t smem = (size_t)blob_al + (size_t)nwg * tc::kABytes + 1024;
-  static size_t attr_smem = 0;
-  if (attr_smem < smem) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<false>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_smem = smem;
-  }
   const int64_t n = a.v1 - a.v0;
   const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
   const int64_t ctas = std::min<int64_t>((tiles + nwg - 1) / nwg, sm_count());
   const unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
-  if (a.prec == NDF_PREC_FP16)
-    tc::query_tc_kernel<true><<<grid, nwg * 128, smem, s>>>(a, nwg);
-  else
-    tc::query_tc_kernel<false><<<grid, nwg * 128, smem, s>>>(a, nwg);
-  NDF_LAUNCH_CHECK();
-  return NDF_OK;
+
+  tc::TcArgs t{};
+  t.q = a;
+  t.n_ref = n_ref;
+  t.out16 = out16;
+  t.ld_out = ld_out;
+  void* scratch = nullptr;
+  double* ref_host_dev = nullptr;
+  if (a.mode == 0) {
+    const int naxis = a.nx + a.ny + a.nz;
+    const size_t fbytes = (size_t)naxis * 2 * tc::kL * sizeof(float);
+    const size_t ebytes = (size_t)n_ref * tc::kERefStride * sizeof(float);
+    const size_t rbytes = refs_dev ? 0 : 3 * sizeof(double);
+    NDF_CUDA_CHECK(cudaMallocAsync(&scratch, fbytes + ebytes + rbytes + 64, s));
+    t.ftab = reinterpret_cast<float*>(scratch);
+    t.erefs = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(scratch) + fbytes);
+    const double* refs = refs_dev;
+    if (!refs) {   // single reference: its coordinates travel as kernel arguments
+      ref_host_dev = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) + fbytes + ebytes);
+      NDF_CUDA_CHECK(cudaMemcpyAsync(ref_host_dev, a.ref, 3 * sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+      refs = ref_host_dev;
+    }
+    const int threads = 128;
+    tc::prep_kernel<<<(naxis + n_ref + threads - 1) / threads, threads, 0, s>>>(
+        a, refs, n_ref, const_cast<float*>(t.ftab), const_cast<float*>(t.erefs));
+    NDF_LAUNCH_CHECK();
+  }
+  int st = a.prec == NDF_PREC_FP16 ? launch_tc_variant<true>(t, nwg, smem, grid, s)
+                                   : launch_tc_variant<false>(t, nwg, smem, grid, s);
+  if (scratch) cudaFreeAsync(scratch, s);
+  return st;
 }
+
+int launch_query_tc(const QueryArgs& a, cudaStream_t s) { return run_tc(a, nullptr, 1, nullptr, 0, s); }
 
 }  // namespace ndf
 
@@ -475,7 +648,7 @@ extern "C" int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_byte
   NDF_REQUIRE(m->params_f32 != nullptr, NDF_ERR_PARAMETER, "null params_f32");
   NDF_REQUIRE(m->tc_format == NDF_PREC_BF16 || m->tc_format == NDF_PREC_FP16, NDF_ERR_PARAMETER,
               "tc_format must be NDF_PREC_BF16 or NDF_PREC_FP16");
-  tc::pack_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
+  tc::pack_zero_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
   NDF_LAUNCH_CHECK();
   tc::pack_fill_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
   NDF_LAUNCH_CHECK();
@@ -486,8 +659,24 @@ extern "C" int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs,
                                     int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
                                     int64_t v0, int64_t v1, uint16_t* out_f16, int64_t ld_out,
                                     void* stream) {
-  (void)m; (void)refs; (void)n_ref; (void)ref_is_mu; (void)nx; (void)ny; (void)nz;
-  (void)v0; (void)v1; (void)out_f16; (void)ld_out; (void)stream;
-  ndf::set_error("ndf_query_grid_multi: not implemented yet");
-  return NDF_ERR_UNSUPPORTED;
+  int st = validate_model(m);
+  if (st) return st;
+  NDF_REQUIRE(n_ref >= 1 && refs != nullptr, NDF_ERR_PARAMETER, "need >= 1 reference");
+  NDF_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, NDF_ERR_PARAMETER, "grid dims must be >= 1");
+  const int64_t V = (int64_t)nx * ny * nz;
+  NDF_REQUIRE(v0 >= 0 && v0 <= v1 && v1 <= V, NDF_ERR_PARAMETER, "vertex range out of bounds");
+  NDF_REQUIRE(ld_out >= v1 - v0, NDF_ERR_PARAMETER, "ld_out smaller than the vertex range");
+  NDF_REQUIRE(out_f16 != nullptr || v0 == v1, NDF_ERR_PARAMETER, "null output");
+  NDF_REQUIRE(m->tc_format == NDF_PREC_BF16 || m->tc_format == NDF_PREC_FP16, NDF_ERR_PARAMETER,
+              "multi-reference queries run on the tensor-core path only");
+  if (v0 == v1) return NDF_OK;
+  QueryArgs a{};
+  a.m = *m;
+  a.g = make_geom(*m);
+  a.mode = 0;
+  a.ref_is_mu = ref_is_mu ? 1 : 0;
+  a.nx = nx; a.ny = ny; a.nz = nz;
+  a.v0 = v0; a.v1 = v1;
+  a.prec = m->tc_format;
+  return run_tc(a, refs, n_ref, out_f16, ld_out, as_stream(stream));
 }
