@@ -30,6 +30,7 @@
 //   * multi-reference queries (BASELINE config 3) embed each query vertex once and
 //     reuse it for every reference (refs' embeddings come from the prep kernel).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "ndf_query.cuh"
@@ -184,37 +185,68 @@ __device__ __forceinline__ void latent_f32(const float* __restrict__ grid, int r
   for (int ch = 0; ch < kC; ++ch) out[ch] = acc[ch];
 }
 
-// Grid-mode embedding of node (ix, iy, iz): raw coords, the per-axis Fourier block
-// from the table written by prep_kernel (fp64 sincos, cast once), the latent part
-// from latent_f32.
+// Per-axis node table written by prep_kernel, one 64-byte row per axis node:
+// [sin/cos of the L octaves (fp64 sincos, cast once) | p (fp32) | i0 | t (fp32) | pad].
+constexpr int kAxisRow = 16;
+static_assert(2 * kL + 4 == kAxisRow, "axis row layout");
+
+// Grid-mode embedding of node (ix, iy, iz): raw coords and the Fourier block come
+// from the per-axis table; the latent cell is computed arithmetically
+// (u = i * (r-1)/(n-1) in fp32) so the latent gathers do not wait for the table
+// loads -- both go to L2 in one round trip (L1 is all SMEM here).
 __device__ __forceinline__ void embed_grid_node(const QueryArgs& a, const float* __restrict__ grid,
-                                                const float* __restrict__ ftab, int64_t v,
-                                                float* e) {
-  const int64_t plane = (int64_t)a.nx * a.ny;
-  const int iz = (int)(v / plane);
-  const int64_t r = v - (int64_t)iz * plane;
-  const int iy = (int)(r / a.nx);
-  const int ix = (int)(r - (int64_t)iy * a.nx);
-  const double p[3] = {node_coord(ix, a.nx), node_coord(iy, a.ny), node_coord(iz, a.nz)};
-  e[0] = (float)p[0];
-  e[1] = (float)p[1];
-  e[2] = (float)p[2];
+                                                const float* __restrict__ ftab, int ix, int iy,
+                                                int iz, const float* lscale, float* e) {
+  const int idx3[3] = {ix, iy, iz};
+  const int res[3] = {a.g.rx, a.g.ry, a.g.rz};
+  const int nn[3] = {a.nx, a.ny, a.nz};
+  int i0[3];
+  float tt[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    // node i of an n-node axis sits at u = i*(r-1)/(n-1); a single-node axis at the
+    // domain centre, u = (r-1)/2 (measures.py:245-247)
+    const float u = nn[ax] > 1 ? (float)idx3[ax] * lscale[ax] : 0.5f * (float)(res[ax] - 1);
+    i0[ax] = min((int)u, res[ax] - 2);
+    tt[ax] = fminf(u - (float)i0[ax], 1.0f);
+  }
+  float acc[kC];
+#pragma unroll
+  for (int ch = 0; ch < kC; ++ch) acc[ch] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+    const float w = (dx ? tt[0] : 1.0f - tt[0]) * (dy ? tt[1] : 1.0f - tt[1]) *
+                    (dz ? tt[2] : 1.0f - tt[2]);
+    const int idx = (i0[0] + dx) + a.g.rx * ((i0[1] + dy) + a.g.ry * (i0[2] + dz));
+    const float4* row = reinterpret_cast<const float4*>(grid + (size_t)idx * kC);
+#pragma unroll
+    for (int q = 0; q < kC / 4; ++q) {
+      const float4 f = __ldg(row + q);
+      acc[4 * q + 0] = fmaf(w, f.x, acc[4 * q + 0]);
+      acc[4 * q + 1] = fmaf(w, f.y, acc[4 * q + 1]);
+      acc[4 * q + 2] = fmaf(w, f.z, acc[4 * q + 2]);
+      acc[4 * q + 3] = fmaf(w, f.w, acc[4 * q + 3]);
+    }
+  }
   const int rows[3] = {ix, a.nx + iy, a.nx + a.ny + iz};
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
-    const float4* t = reinterpret_cast<const float4*>(ftab + (size_t)rows[ax] * (2 * kL));
+    const float4* t = reinterpret_cast<const float4*>(ftab + (size_t)rows[ax] * kAxisRow);
 #pragma unroll
-    for (int q = 0; q < (2 * kL) / 4; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const float4 f = __ldg(t + q);
       const float fv[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int j = 4 * q + u;            // j = 2*octave + (0 sin | 1 cos)
-        e[3 + 6 * (j >> 1) + 2 * ax + (j & 1)] = fv[u];
+        const int j = 4 * q + u;
+        if (j < 2 * kL) e[3 + 6 * (j >> 1) + 2 * ax + (j & 1)] = fv[u];  // 2*octave + sin|cos
+        else if (j == 2 * kL) e[ax] = fv[u];
       }
     }
   }
-  latent_f32(grid, a.g.rx, a.g.ry, a.g.rz, p[0], p[1], p[2], e + 3 + 6 * kL);
+#pragma unroll
+  for (int ch = 0; ch < kC; ++ch) e[3 + 6 * kL + ch] = acc[ch];
 }
 
 // Points-mode embedding (NdfModel.forward): fp64 sincos per point, fp32 latent.
@@ -242,12 +274,22 @@ __device__ __forceinline__ void embed_point_tc(const QueryArgs& a, const float* 
 
 struct TcArgs {
   QueryArgs q;
-  const float* ftab;      // grid mode: (nx+ny+nz) x 2L Fourier table
+  const float* ftab;      // grid mode: (nx+ny+nz) x kAxisRow per-axis node table
   const float* erefs;     // grid mode: n_ref x kERefStride reference embeddings
   int n_ref;
   uint16_t* out16;        // multi-ref output (fp16), rows of ld_out
   int64_t ld_out;
+  long long* trace;       // debug: per-phase clock64 stamps of CTA 0 (NULL = off)
+  int stagger;            // cycles between warpgroup start times (de-phases the WGs)
 };
+
+// debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
+constexpr int kTraceTiles = 32, kTraceEvents = 12;
+#define NDF_TRACE(ev)                                                                    \
+  do {                                                                                   \
+    if (t.trace && blockIdx.x == 0 && wtid == 0 && tcount < kTraceTiles)                  \
+      t.trace[(wg * kTraceTiles + tcount) * kTraceEvents + (ev)] = clock64();           \
+  } while (0)
 
 // One MMA stage: K/16 tcgen05.mma steps into the warpgroup's accumulator, committed
 // to its mbarrier.  Issued by one thread.
@@ -279,6 +321,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   uint8_t* abufs = smem + ((lay.blob_bytes + 1023) & ~1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + nwg * kABytes);   // [0] weights, [1+w]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  float* eref_s = reinterpret_cast<float*>(bars + 16);      // single-ref grid: e_ref in SMEM
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -333,14 +376,43 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   const float* grid_q = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
   const int bar_id = 1 + wg;
   const int n_ref = KIND == kGridMulti ? t.n_ref : 1;
+  if (KIND == kGridSingle) {
+    if (tid < kERefStride) eref_s[tid] = t.erefs[tid];
+    __syncthreads();
+  }
 
-  for (int64_t tile = (int64_t)blockIdx.x * nwg + wg; tile < n_tiles; tile += stride) {
+  // De-phase the warpgroups so one WG's encoder / MMA waits overlap another's
+  // MUFU-bound epilogue instead of all four contending for the same unit at once.
+  if (t.stagger > 0) {
+    const long long c0 = clock64();
+    while (clock64() - c0 < (long long)wg * t.stagger) {
+    }
+  }
+  const float lscale[3] = {a.nx > 1 ? (float)(a.g.rx - 1) / (float)(a.nx - 1) : 0.0f,
+                           a.ny > 1 ? (float)(a.g.ry - 1) / (float)(a.ny - 1) : 0.0f,
+                           a.nz > 1 ? (float)(a.g.rz - 1) / (float)(a.nz - 1) : 0.0f};
+  int tcount = 0;
+  for (int64_t tile = (int64_t)blockIdx.x * nwg + wg; tile < n_tiles; tile += stride, ++tcount) {
+    NDF_TRACE(0);
     const int64_t vloc = tile * kTileM + wtid;   // local vertex index
     const bool valid = vloc < n;
     // ---- K1: embed the query vertex once -----------------------------------------
     float eq[kE];
     if (valid && KIND != kPoints) {
-      embed_grid_node(a, grid_q, t.ftab, a.v0 + vloc, eq);
+      // vertex -> (ix, iy, iz): one 32-bit division pair for the tile's first vertex
+      // (warp-uniform), then carry the thread's offset along x (x fastest).
+      const uint32_t vb = (uint32_t)(a.v0 + tile * kTileM);
+      const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
+      int iz = (int)(vb / nxy);
+      const uint32_t rem = vb - (uint32_t)iz * nxy;
+      int iy = (int)(rem / (uint32_t)a.nx);
+      int ix = (int)(rem - (uint32_t)iy * (uint32_t)a.nx) + wtid;
+      while (ix >= a.nx) {
+        ix -= a.nx;
+        if (++iy == a.ny) { iy = 0; ++iz; }
+      }
+      embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);
+      NDF_TRACE(8);
     } else if (valid) {
       embed_point_tc(a, a.m.grid_nu, a.p_nu + 3 * (a.v0 + vloc), eq);
     } else {
@@ -350,11 +422,12 @@ query_tc_kernel(const TcArgs t, const int nwg) {
     for (int r = 0; r < n_ref; ++r) {
       // ---- bias of layer 0 -> accumulator (tcgen05.st); the MMAs then accumulate ----
       preload_bias(tmem_row, vecs);
+      NDF_TRACE(9);
       // ---- merge -> A ------------------------------------------------------------
       auto fq = [&](int i) { return eq[i]; };
       if constexpr (KIND != kPoints) {
         const float* er = t.erefs + (size_t)r * kERefStride;
-        auto fr = [&](int i) { return __ldg(er + i); };
+        auto fr = [&](int i) { return KIND == kGridSingle ? eref_s[i] : __ldg(er + i); };
         if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)      // symmetric: role does not matter
           write_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(a_addr, wtid, 0, fr, fq, lay.kin);
         else if (a.ref_is_mu)
@@ -373,10 +446,12 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         auto fm = [&](int i) { return em[i]; };
         write_input_row<F16, -1>(a_addr, wtid, a.m.merge, fm, fq, lay.kin);
       }
+      NDF_TRACE(11);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_proxy_async();
       tc_fence_before();
       named_bar(bar_id, 128);
+      NDF_TRACE(1);
       // ---- K2: hidden layers on the tensor cores --------------------------------------
       for (int l = 0; l < lay.H; ++l) {
         if (wtid == 0) {
@@ -387,6 +462,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
+        NDF_TRACE(2 + 2 * l);
         const bool next_hidden = l + 1 < lay.H;
         const float4* nbias4 = reinterpret_cast<const float4*>(vecs + (l + 1) * kHid);
 #pragma unroll 1
@@ -421,6 +497,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         fence_proxy_async();
         tc_fence_before();
         named_bar(bar_id, 128);
+        NDF_TRACE(3 + 2 * l);
       }
       // ---- output layer (128 -> 1) as a 16-column MMA ---------------------------------
       if (wtid == 0)
@@ -428,6 +505,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
       mbar_wait(bar, phase);
       phase ^= 1;
       tc_fence_after();
+      NDF_TRACE(10);
       uint32_t zr;
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                    : "=r"(zr) : "r"(tmem_row));
@@ -461,14 +539,20 @@ __global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, fl
     if (tid < a.nx) { ax = 0; i = tid; n = a.nx; }
     else if (tid < a.nx + a.ny) { ax = 1; i = tid - a.nx; n = a.ny; }
     else { ax = 2; i = tid - a.nx - a.ny; n = a.nz; }
-    (void)ax;
     const double p = fmin(fmax(node_coord(i, n), -1.0), 1.0);
+    const int res = ax == 0 ? a.g.rx : (ax == 1 ? a.g.ry : a.g.rz);
+    const AxisCoord lc = level_coord(p, res);
+    float* row = ftab + (size_t)tid * kAxisRow;
+    row[2 * kL] = (float)p;
+    row[2 * kL + 1] = __int_as_float(lc.i0);
+    row[2 * kL + 2] = (float)lc.t;
+    row[2 * kL + 3] = 0.0f;
     double scale = 3.141592653589793;
     for (int o = 0; o < kL; ++o) {
       double s, c;
       sincos(dmul(scale, p), &s, &c);
-      ftab[tid * 2 * kL + 2 * o] = (float)s;
-      ftab[tid * 2 * kL + 2 * o + 1] = (float)c;
+      row[2 * o] = (float)s;
+      row[2 * o + 1] = (float)c;
       scale = scale * 2.0;
     }
   } else if (tid < naxis + n_ref) {
@@ -576,6 +660,8 @@ static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned
 
 // Grid / points query on the tensor cores; refs (device, n_ref x 3) and out16 are
 // only used by the multi-reference entry point.
+static long long* g_trace = nullptr;   // debug hook (ndf_debug_tc_trace)
+
 static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_t* out16,
                   int64_t ld_out, cudaStream_t s) {
   std::string why;
@@ -598,11 +684,22 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
   t.n_ref = n_ref;
   t.out16 = out16;
   t.ld_out = ld_out;
+  t.trace = g_trace;
+  {
+    static int stagger = -1;
+    if (stagger < 0) {
+      const char* e = getenv("NDF_TC_STAGGER");
+      stagger = e ? atoi(e) : 1500;
+    }
+    t.stagger = stagger;
+  }
   void* scratch = nullptr;
   double* ref_host_dev = nullptr;
   if (a.mode == 0) {
+    NDF_REQUIRE((int64_t)a.nx * a.ny * a.nz < (1LL << 32), NDF_ERR_UNSUPPORTED,
+                "tensor-core grid query supports < 2^32 vertices");
     const int naxis = a.nx + a.ny + a.nz;
-    const size_t fbytes = (size_t)naxis * 2 * tc::kL * sizeof(float);
+    const size_t fbytes = (size_t)naxis * tc::kAxisRow * sizeof(float);
     const size_t ebytes = (size_t)n_ref * tc::kERefStride * sizeof(float);
     const size_t rbytes = refs_dev ? 0 : 3 * sizeof(double);
     NDF_CUDA_CHECK(cudaMallocAsync(&scratch, fbytes + ebytes + rbytes + 64, s));
@@ -631,6 +728,10 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) { return run_tc(a, nullp
 }  // namespace ndf
 
 using namespace ndf;
+
+// Debug only (not part of the C-ABI header): subsequent tensor-core queries record
+// CTA 0's per-phase clock64() stamps into buf[4 * 32 * 12] (NULL disables).
+extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 
 extern "C" size_t ndf_tc_blob_bytes(const ndf_model_desc* m) {
   if (!m || !tc_supported(*m, nullptr)) return 0;
