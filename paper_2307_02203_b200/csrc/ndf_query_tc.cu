@@ -285,6 +285,11 @@ struct TcArgs {
 
 // debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
 constexpr int kTraceTiles = 32, kTraceEvents = 12;
+#define NDF_TRACE_AT(slot_, ev)                                                          \
+  do {                                                                                   \
+    if (t.trace && blockIdx.x == 0 && wtid == 0 && (slot_) < kTraceTiles)                 \
+      t.trace[(wg * kTraceTiles + (slot_)) * kTraceEvents + (ev)] = clock64();          \
+  } while (0)
 #define NDF_TRACE(ev)                                                                    \
   do {                                                                                   \
     if (t.trace && blockIdx.x == 0 && wtid == 0 && tcount < kTraceTiles)                  \
@@ -529,6 +534,320 @@ query_tc_kernel(const TcArgs t, const int nwg) {
                  "r"(tmem_cols));
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised schedule (NDF_TC_SCHEDULE=ws).  Four TMEM-accumulator / A-buffer slots.
+//   WG0, WG1 -- epilogue warpgroups: drain accumulators (tcgen05.ld, software-
+//               pipelined one 32-column chunk ahead), bias + activation, write the
+//               next A operand, issue the next MMA.  Each owns two slots and
+//               alternates between them with slot B running two stages behind slot
+//               A, so (i) its epilogue on one slot hides the MMA of the other and
+//               (ii) the two slots are released at different times.
+//   WG2, WG3 -- producer warpgroups: embed the next query tile and pack its merged
+//               16-bit layer-0 rows in registers *before* the slot frees, then only
+//               store them (14 x 16 B per row) and issue the layer-0 MMA.
+// Slot s is shared by epilogue WG (s & 1) and producer WG 2 + (s & 1); the pair
+// walks the deterministic item sequence j = tile_k * n_ref + r, item j in slot
+// pair[j & 1].  Synchronisation is mbarrier-only: acc_full[s] (tcgen05.commit after
+// each MMA stage) and slot_free[s] (epilogue WG after reading the output column).
+constexpr int kSlots = 4;
+constexpr int kKinMax = 128;
+
+template <bool F16, int MERGE, class FA, class FB>
+__device__ __forceinline__ void pack_input_row(int merge, FA ea, FB eb, int kin, uint32_t* pk) {
+#pragma unroll
+  for (int kg = 0; kg < kKinMax / 8; ++kg) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i0 = 8 * kg + 2 * q;
+      pk[4 * kg + q] = (8 * kg < kin)
+          ? pack2<F16>(merged_value<MERGE>(merge, i0, ea, eb), merged_value<MERGE>(merge, i0 + 1, ea, eb))
+          : 0u;
+    }
+  }
+}
+
+template <bool F16, bool SILU>
+__device__ __forceinline__ void epilogue_chunk(const float* v, const float4* b4, int c0,
+                                               int act, uint32_t a_addr, int row) {
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const float4 ba = b4[(c0 >> 2) + 2 * jj];
+    const float4 bb = b4[(c0 >> 2) + 2 * jj + 1];
+    const float x[8] = {v[8 * jj] + ba.x, v[8 * jj + 1] + ba.y, v[8 * jj + 2] + ba.z,
+                        v[8 * jj + 3] + ba.w, v[8 * jj + 4] + bb.x, v[8 * jj + 5] + bb.y,
+                        v[8 * jj + 6] + bb.z, v[8 * jj + 7] + bb.w};
+    uint32_t p[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x0 = x[2 * q], x1 = x[2 * q + 1];
+      if constexpr (SILU)     // x = z/2 (weights pre-scaled): silu(z) = x + x*tanh(x)
+        p[q] = pack2<F16>(fmaf(x0, tanh_fast(x0), x0), fmaf(x1, tanh_fast(x1), x1));
+      else
+        p[q] = pack2<F16>(act_f32(act, x0), act_f32(act, x1));
+    }
+    st_shared_v4(a_addr + canon_off(row, c0 + 8 * jj, kSboA), p[0], p[1], p[2], p[3]);
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <bool F16, bool SILU, int KIND>
+__global__ void __launch_bounds__(512, 1)
+query_ws_kernel(const TcArgs t) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const QueryArgs& a = t.q;
+  const Layout lay = make_layout(a.m);
+  uint8_t* wblob = smem;
+  uint8_t* abufs = smem + ((lay.blob_bytes + 1023) & ~1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + kSlots * kABytes);
+  uint64_t* wbar = &bars[0];
+  uint64_t* acc_full = &bars[1];            // [kSlots]
+  uint64_t* slot_free = &bars[1 + kSlots];  // [kSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  float* eref_s = reinterpret_cast<float*>(bars + 16);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int wg = warp >> 2;
+  const int wtid = tid & 127;
+  const float* vecs = reinterpret_cast<const float*>(wblob + lay.vec_off);
+
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&slot_free[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (KIND == kGridSingle && tid < kERefStride) eref_s[tid] = t.erefs[tid];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    mbar_expect_tx(wbar, (uint32_t)lay.blob_bytes);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.m.params_tc);
+    for (int off = 0; off < lay.blob_bytes; off += 32768)
+      bulk_g2s(wblob + off, src + off, (uint32_t)min(32768, lay.blob_bytes - off), wbar);
+  }
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t w_addr = smem_u32(wblob);
+  const uint32_t ab_fmt = F16 ? 0u : 1u;
+  const uint32_t idesc_base = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
+                              ((uint32_t)(kTileM >> 4) << 24);
+  const uint32_t idesc = idesc_base | ((uint32_t)(kHid >> 3) << 17);
+  const uint32_t idesc_out = idesc_base | ((uint32_t)(kOutN >> 3) << 17);
+  const uint32_t sbo_w0 = (uint32_t)(lay.kin / 8) * 128;
+
+  const int64_t n = a.v1 - a.v0;
+  const int64_t n_tiles = (n + kTileM - 1) / kTileM;
+  const int n_ref = KIND == kGridMulti ? t.n_ref : 1;
+  const int pairid = wg & 1;                               // slot pair {pairid, pairid + 2}
+  const int pair_slots[2] = {pairid, pairid + 2};
+  const int64_t tile_first = (int64_t)blockIdx.x * 2 + pairid;
+  const int64_t tile_stride = (int64_t)gridDim.x * 2;
+  const int64_t my_tiles =
+      tile_first < n_tiles ? (n_tiles - tile_first + tile_stride - 1) / tile_stride : 0;
+  const int64_t n_items = my_tiles * n_ref;
+  const int bar_id = 1 + wg;
+  const float* grid_q = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
+
+  if (wg >= 2) {
+    // ======================= producer warpgroup ==================================
+    const float lscale[3] = {a.nx > 1 ? (float)(a.g.rx - 1) / (float)(a.nx - 1) : 0.0f,
+                             a.ny > 1 ? (float)(a.g.ry - 1) / (float)(a.ny - 1) : 0.0f,
+                             a.nz > 1 ? (float)(a.g.rz - 1) / (float)(a.nz - 1) : 0.0f};
+    uint32_t free_ph[2] = {0u, 0u};
+    float eq[kE];
+    bool weights_ready = false;
+    for (int64_t j = 0; j < n_items; ++j) {
+      const int64_t k = j / n_ref;
+      const int r = (int)(j - k * n_ref);
+      const int si = (int)(j & 1);
+      const int s = pair_slots[si];
+      const int64_t tile = tile_first + k * tile_stride;
+      const int64_t vloc = tile * kTileM + wtid;
+      const bool valid = vloc < n;
+      NDF_TRACE_AT((int)j, 0);
+      if (r == 0) {                                   // new tile: embed the query vertex
+        if (valid && KIND != kPoints) {
+          const uint32_t vb = (uint32_t)(a.v0 + tile * kTileM);
+          const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
+          int iz = (int)(vb / nxy);
+          const uint32_t rem = vb - (uint32_t)iz * nxy;
+          int iy = (int)(rem / (uint32_t)a.nx);
+          int ix = (int)(rem - (uint32_t)iy * (uint32_t)a.nx) + wtid;
+          while (ix >= a.nx) {
+            ix -= a.nx;
+            if (++iy == a.ny) { iy = 0; ++iz; }
+          }
+          embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);
+        } else if (valid) {
+          embed_point_tc(a, a.m.grid_nu, a.p_nu + 3 * (a.v0 + vloc), eq);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
+        }
+      }
+      // merged layer-0 row, packed to 16 bit, ready before the slot frees
+      uint32_t pk[kKinMax / 2];
+      auto fq = [&](int i) { return eq[i]; };
+      if constexpr (KIND != kPoints) {
+        const float* er = t.erefs + (size_t)r * kERefStride;
+        auto fr = [&](int i) { return KIND == kGridSingle ? eref_s[i] : __ldg(er + i); };
+        if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)
+          pack_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(0, fr, fq, lay.kin, pk);
+        else if (a.ref_is_mu)
+          pack_input_row<F16, -1>(a.m.merge, fr, fq, lay.kin, pk);
+        else
+          pack_input_row<F16, -1>(a.m.merge, fq, fr, lay.kin, pk);
+      } else {
+        float em[kE];
+        if (valid) {
+          const int64_t im = a.n_mu == 1 ? 0 : a.v0 + vloc;
+          embed_point_tc(a, a.m.grid_mu, a.p_mu + 3 * im, em);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kE; ++i) em[i] = 0.0f;
+        }
+        auto fm = [&](int i) { return em[i]; };
+        pack_input_row<F16, -1>(a.m.merge, fm, fq, lay.kin, pk);
+      }
+      NDF_TRACE_AT((int)j, 1);
+      if (!weights_ready) {
+        mbar_wait(wbar, 0);
+        weights_ready = true;
+      }
+      if (j >= 2) {                                   // slot must be drained first
+        mbar_wait(&slot_free[s], free_ph[si]);
+        free_ph[si] ^= 1u;
+      }
+      NDF_TRACE_AT((int)j, 2);
+      const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+#pragma unroll
+      for (int kg = 0; kg < kKinMax / 8; ++kg)
+        if (8 * kg < lay.kin)
+          st_shared_v4(a_addr + canon_off(wtid, 8 * kg, kSboA), pk[4 * kg], pk[4 * kg + 1],
+                       pk[4 * kg + 2], pk[4 * kg + 3]);
+      fence_proxy_async();
+      tc_fence_before();
+      named_bar(bar_id, 128);
+      if (wtid == 0)
+        issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr, lay.kin, sbo_w0, idesc,
+                    &acc_full[s], 0u);
+      NDF_TRACE_AT((int)j, 3);
+    }
+  } else {
+    // ======================= epilogue warpgroup ==================================
+    mbar_wait(wbar, 0);
+    const float bias_out = vecs[lay.H * kHid];
+    const int n_st = lay.H + 1;                  // stages per item: H hidden + output
+    uint32_t acc_ph[2] = {0u, 0u};
+    int64_t item[2] = {0, 1};                    // current item of each slot
+    int stage[2] = {0, -2};                      // slot B runs two stages behind slot A
+    for (;;) {
+      bool any = false;
+      for (int si = 0; si < 2; ++si) {
+        if (stage[si] < 0) { ++stage[si]; any = true; continue; }   // start-up skew
+        const int64_t j = item[si];
+        if (j >= n_items) continue;
+        any = true;
+        const int st = stage[si];
+        const int s = pair_slots[si];
+        const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(s * kHid);
+        const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+        mbar_wait(&acc_full[s], acc_ph[si]);
+        acc_ph[si] ^= 1u;
+        tc_fence_after();
+        NDF_TRACE_AT((int)(j >> 1), si * 5 + min(st, 4));
+        if (st < lay.H) {
+          // ---- hidden layer st: drain, bias + activation, write next A, next MMA ----
+          const float4* b4 = reinterpret_cast<const float4*>(vecs + st * kHid);
+          float va[32], vb[32];
+          tmem_ld32_nowait(tmem_row, va);
+          tmem_wait_ld();
+          tmem_ld32_nowait(tmem_row + 32u, vb);
+          epilogue_chunk<F16, SILU>(va, b4, 0, a.m.activation, a_addr, wtid);
+          tmem_wait_ld();
+          tmem_ld32_nowait(tmem_row + 64u, va);
+          epilogue_chunk<F16, SILU>(vb, b4, 32, a.m.activation, a_addr, wtid);
+          tmem_wait_ld();
+          tmem_ld32_nowait(tmem_row + 96u, vb);
+          epilogue_chunk<F16, SILU>(va, b4, 64, a.m.activation, a_addr, wtid);
+          tmem_wait_ld();
+          epilogue_chunk<F16, SILU>(vb, b4, 96, a.m.activation, a_addr, wtid);
+          fence_proxy_async();
+          tc_fence_before();
+          named_bar(bar_id, 128);
+          if (wtid == 0) {
+            if (st + 1 < lay.H)
+              issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr,
+                          w_addr + lay.w0_bytes + st * lay.wh_bytes, kHid, kSboA, idesc,
+                          &acc_full[s], 0u);
+            else
+              issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr + lay.wout_off,
+                          kHid, kSboA, idesc_out, &acc_full[s], 0u);
+          }
+          stage[si] = st + 1;
+        } else {
+          // ---- output column: head, store, release the slot ---------------------------
+          uint32_t zr;
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                       : "=r"(zr) : "r"(tmem_row));
+          tmem_wait_ld();
+          tc_fence_before();
+          const int64_t k = j / n_ref;
+          const int r = (int)(j - k * n_ref);
+          const int64_t vloc = (tile_first + k * tile_stride) * kTileM + wtid;
+          if (vloc < n) {
+            const float z = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
+            if (t.out16) {
+              const __half hz = __float2half_rn(z);
+              t.out16[(size_t)r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&hz);
+            } else {
+              a.out[vloc] = z;
+            }
+          }
+          named_bar(bar_id, 128);
+          if (wtid == 0) mbar_arrive(&slot_free[s]);
+          NDF_TRACE_AT((int)(j >> 1), 10 + si);
+          item[si] = j + 2;
+          stage[si] = 0;
+        }
+        (void)n_st;
+      }
+      if (!any) break;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+}
+
 // ---- per-query prep: per-axis Fourier table + reference embeddings ------------
 __global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, float* ftab,
                             float* erefs) {
@@ -635,9 +954,28 @@ static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid,
   if (attr < smem) {
     NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<F16, SILU, KIND>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_ws_kernel<F16, SILU, KIND>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
+  // Schedule: "classic" (default; 4 symmetric warpgroups, one slot each) or "ws"
+  // (warp-specialised producer / epilogue warpgroups -- currently slower: the
+  // epilogue warps are MUFU-latency bound with only two per SM sub-partition).
+  static int classic = -1;
+  if (classic < 0) {
+    const char* e = getenv("NDF_TC_SCHEDULE");
+    classic = (e && e[0] == 'w') ? 0 : 1;
+  }
+  if (classic || nwg != 4) {
+    tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
+  } else {
+    // warp-specialised: one CTA covers 2 slot pairs; grid from the tile count
+    const int64_t n = t.q.v1 - t.q.v0;
+    const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
+    const unsigned g2 = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((tiles + 3) / 4, sm_count()));
+    tc::query_ws_kernel<F16, SILU, KIND><<<g2, 512, smem, s>>>(t);
+  }
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }
