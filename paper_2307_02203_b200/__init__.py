@@ -15,11 +15,11 @@ from .errors import (ConfigError, CorruptFileError, DataError, DegenerateSampleE
                      ParameterError, ShapeError, TrainingError, UnknownVariableError)
 from .measures import (CorrelationMeasure, FieldGrid, digamma, gaussian_mi_analytic,
                        grid_positions, ground_truth_field, ground_truth_field_device, ksg_mi,
-                       ksg_rows, load_field_grid, pearson, pearson_against, pearson_rowwise,
-                       save_field_grid)
+                       ksg_rows, load_field_grid, pair_estimators_device, pearson,
+                       pearson_against, pearson_rowwise, save_field_grid)
 from .model import DeviceModel, ModelSpec, NdfModel, load_model, save_model
 from .service import (ROLE_MU, ROLE_NU, benchmark, difference_field, matrix_reconstruct,
-                      reconstruct_field, reconstruct_field_device)
+                      reconstruct_field, reconstruct_field_device, reconstruct_multi_device)
 
 __version__ = "0.1.0"
 
@@ -30,7 +30,8 @@ __all__ = [
     "ParameterError", "ROLE_MU", "ROLE_NU", "ShapeError", "TrainingError", "UnknownVariableError",
     "benchmark", "difference_field", "digamma", "gaussian_mi_analytic", "grid_positions",
     "ground_truth_field", "ground_truth_field_device", "ksg_mi", "ksg_rows", "load_ensemble",
-    "load_field_grid", "load_model", "matrix_reconstruct", "pearson", "pearson_against",
-    "pearson_rowwise", "reconstruct_field", "reconstruct_field_device", "sample_at",
+    "load_field_grid", "load_model", "matrix_reconstruct", "pair_estimators_device", "pearson",
+    "pearson_against", "pearson_rowwise", "reconstruct_field", "reconstruct_field_device",
+    "reconstruct_multi_device", "sample_at",
     "sample_many", "save_ensemble", "save_field_grid", "save_model",
 ]

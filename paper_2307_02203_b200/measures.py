@@ -372,3 +372,45 @@ def load_field_grid(path) -> FieldGrid:
     if len(payload) != x * y * z * 4:
         raise CorruptFileError(f"payload holds {len(payload) // 4} values, expected {x * y * z}")
     return FieldGrid((x, y, z), np.frombuffer(payload, dtype="<f4").copy())
+
+
+def pair_estimators_device(field_obj, variable: str, pa, pb, k: int = 8,
+                           measures=("pearson", "ksg_mi")):
+    """Bulk estimator pairs (BASELINE config 4 / training-target generation).
+
+    For vertex pairs (pa[p], pb[p]) of one variable's node grid computes Pearson r
+    (fp64, measures.py:111-133) and/or KSG MI (fp64, measures.py:173-203) on the
+    GPU from a vertex-major copy of the ensemble.  Replaces the per-pair loop of
+    training._targets (training.py:111-119).  Returns {name: CUDA fp64 tensor}.
+    """
+    import torch
+    dev_ens = _device_view(field_obj, variable)
+    dev = dev_ens.device
+    V, M = dev_ens.node_count, dev_ens.member_count
+    ta = torch.as_tensor(np.ascontiguousarray(pa, dtype=np.int64)).to(dev)
+    tb = torch.as_tensor(np.ascontiguousarray(pb, dtype=np.int64)).to(dev)
+    if ta.shape != tb.shape or ta.dim() != 1:
+        raise ParameterError("pair index arrays must be equal-length vectors")
+    if ta.numel() and (int(torch.minimum(ta.min(), tb.min())) < 0
+                       or int(torch.maximum(ta.max(), tb.max())) >= V):
+        raise ParameterError("pair index out of range")
+    n = int(ta.numel())
+    Xv = dev_ens.vertex_major()
+    stream = N.stream_handle(dev)
+    out = {}
+    if "pearson" in measures:
+        r = torch.empty(n, dtype=torch.float64, device=dev)
+        N.call("ndf_pearson_pairs", N.ptr(Xv), M, V, N.ptr(ta), N.ptr(tb), n, N.ptr(r), stream)
+        out["pearson"] = r
+    if "ksg_mi" in measures:
+        if not 1 <= k <= M - 1:
+            raise ParameterError(f"need 1 <= k <= N-1, got k={k}, N={M}")
+        jit, psi = _KsgTables.get(dev, M)
+        mi = torch.empty(n, dtype=torch.float64, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        N.call("ndf_ksg_pairs", N.ptr(Xv), M, V, N.ptr(ta), N.ptr(tb), n, k, N.ptr(jit),
+               N.ptr(psi), _KsgTables.psi_km(k, M), N.ptr(mi), None, None, N.ptr(status), stream)
+        if int(status.item()):
+            raise ParameterError("digamma defined here for positive arguments only")
+        out["ksg_mi"] = mi
+    return out

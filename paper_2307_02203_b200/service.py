@@ -173,3 +173,36 @@ def benchmark(model: NdfModel, field_obj, ref, dims, repetitions: int = 3, k: in
     mi_s = mi_sub * (n_points / mi_points)
     return BenchmarkReport(dims, repetitions, ndf_s, pearson_s, mi_s, mi_points,
                            mi_points < n_points, repetitions > 1)
+
+
+def reconstruct_multi_device(model: NdfModel, refs, role: str = ROLE_MU, dims=(64, 64, 64),
+                             v0: int = 0, v1: int | None = None, out=None):
+    """Dependence cube of several reference points: fp16 CUDA tensor (n_ref, v1 - v0).
+
+    BASELINE config 3 (64 references x 1.76 M vertices per model).  The batched
+    form of the reference's per-reference loop (service.py:97-125): each query
+    vertex is embedded once and reused for every reference; values equal the
+    single-reference query's fp32 result rounded to fp16.
+    """
+    import torch
+    _check_role(role)
+    dims = _check_dims(dims)
+    V = dims[0] * dims[1] * dims[2]
+    v1 = V if v1 is None else int(v1)
+    if not 0 <= v0 <= v1 <= V:
+        raise ParameterError("vertex range out of bounds")
+    if model.spec.precision not in ("bf16", "fp16"):
+        raise ParameterError("multi-reference queries run on the tensor-core path "
+                             "(precision 'fp16' or 'bf16')")
+    st = model.device_state()
+    refs_np = np.ascontiguousarray(np.asarray(refs, dtype=np.float64).reshape(-1, 3))
+    n_ref = refs_np.shape[0]
+    drefs = torch.from_numpy(refs_np).to(st.device)
+    if out is None:
+        out = torch.empty((n_ref, v1 - v0), dtype=torch.float16, device=st.device)
+    if out.dtype != torch.float16 or out.shape[0] < n_ref or out.stride(1) != 1:
+        raise ParameterError("out must be a row-major float16 tensor with >= n_ref rows")
+    N.call("ndf_query_grid_multi", ctypes_ref(st.desc), N.ptr(drefs), n_ref,
+           1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], v0, v1, N.ptr(out),
+           out.stride(0), N.stream_handle(st.device))
+    return out

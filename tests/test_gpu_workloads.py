@@ -1,0 +1,92 @@
+"""GPU tests of the batched workloads: multi-reference cube (config 3), bulk estimator
+pairs (config 4) and the single-rank NCCL path of the sharded query."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2307_02203_b200 as ndf  # noqa: E402
+from oracle import ndf_oracle as O  # noqa: E402
+from paper_2307_02203_b200 import workloads as W  # noqa: E402
+
+
+@pytest.mark.parametrize("precision", ["fp16", "bf16"])
+def test_multi_reference_cube_equals_single_queries(precision):
+    dims = (70, 40, 6)
+    spec = ndf.ModelSpec.baseline(dims, 4, precision=precision, grid_init=1.0)
+    model = ndf.NdfModel.build(spec, seed=3)
+    rng = np.random.default_rng(0)
+    refs = np.concatenate([rng.uniform(-1, 1, (5, 3)), [[-1.0, 1.0, 0.2]]])
+    V = int(np.prod(dims))
+    cube = ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims).cpu()
+    assert cube.shape == (len(refs), V) and cube.dtype == torch.float16
+    for r, ref in enumerate(refs):
+        single = ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, dims).cpu()
+        assert torch.equal(cube[r], single.to(torch.float16))
+    # vertex sub-range into a strided output
+    out = torch.zeros((len(refs), 2000), dtype=torch.float16, device="cuda")
+    ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims, 1000, 2500, out=out)
+    assert torch.equal(out[:, :1500].cpu(), cube[:, 1000:2500])
+
+
+def test_multi_reference_oracle_spot_check():
+    w = W.CONFIGS[0]
+    model = W.build_model(w, seed=0, grid_init=1.0).with_precision("fp16")
+    refs = np.array([w.ref_position(), (0.5, -0.5, 1.0), (-1.0, -1.0, -1.0)])
+    cube = ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, w.dims).float().cpu().numpy()
+    om = O.OracleModel(6, model.grid_mu, model.grid_nu, model.weights, model.biases,
+                       model.spec.merge, model.spec.activation, model.spec.head_kind)
+    for r, ref in enumerate(refs):
+        want = O.reconstruct_field(om, ref, w.dims)
+        assert np.max(np.abs(cube[r] - want)) <= 1e-2
+
+
+def test_bulk_pairs_vs_oracle():
+    w = W.Workload("c4_small", (30, 24, 4), 400, (8, 8, 2), 4, "fp16", "ksg_mi", nonlinear=True,
+                   ref_vertex=(15, 12, 2), seed=2311)
+    ens = W.generate_device(w)
+    pa, pb = W.pair_list(w, count=300, seed=2)
+    pa[0] = pb[0]
+    res = ndf.pair_estimators_device(ens, "v", pa, pb, k=8)
+    X = ens.X.reshape(w.members, -1).cpu().numpy()
+    r = res["pearson"].cpu().numpy()
+    mi = res["ksg_mi"].cpu().numpy()
+    want_r = O.pearson_rowwise(X[:, pa].T, X[:, pb].T)
+    assert r[0] == 1.0
+    assert np.max(np.abs(r - want_r)) <= 1e-12
+    for p in range(0, 300, 11):
+        assert mi[p] == O.ksg_mi(X[:, pa[p]].astype(np.float64), X[:, pb[p]].astype(np.float64), 8)
+    with pytest.raises(ndf.ParameterError):
+        ndf.pair_estimators_device(ens, "v", [0], [w.n_vertices], k=8)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_sharded_query_single_rank_nccl():
+    import torch.distributed as dist
+    from paper_2307_02203_b200.parallel import reconstruct_field_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        w = W.CONFIGS[0]
+        model = W.build_model(w, seed=0, grid_init=1.0).with_precision("fp16")
+        got = reconstruct_field_sharded(model, w.ref_position(), ndf.ROLE_MU, w.dims)
+        want = ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
+        assert torch.equal(got, want)
+    finally:
+        dist.destroy_process_group()
