@@ -12,9 +12,12 @@
 // host table built with the reference formula and the mean uses NumPy's
 // pairwise summation order, so MI is reproduced bit for bit as well.
 //
-// One CTA per pair; the jittered vectors and their sorted copies live in SMEM;
-// each thread keeps the running (k+1)-smallest distances of 4 points in
-// registers while streaming all j from SMEM (broadcast reads).
+// One CTA per pair.  The jittered vectors live in SMEM sorted by a' (with b' in the
+// same order) and b' sorted on its own.  Each point's (k+1)-NN scan walks outward
+// in a'-order from its own position and stops once |a'_i - a'_j| alone reaches the
+// running (k+1)-th distance -- typically ~sqrt(kM) candidates instead of M -- and
+// the marginal counts are two binary searches per axis.  For reference-vs-all
+// fields the jittered reference is sorted once per query (ksg_prep_ref_kernel).
 #include <algorithm>
 
 #include "ndf_common.cuh"
@@ -22,7 +25,6 @@
 namespace ndf {
 
 constexpr int kKsgThreads = 256;
-constexpr int kKsgPts = 4;          // points per thread per sweep
 
 struct KsgArgs {
   int mode;                   // 0 ref-vs-node-columns, 1 fp64 rows, 2 vertex-major pairs
@@ -46,6 +48,8 @@ struct KsgArgs {
   int32_t* counts;
   int32_t* status;
   int P;                      // pow2 >= M (sort width)
+  const double* sa_ref;       // mode 0: jittered reference sorted (P, +inf padded)
+  const int* perm_ref;        // mode 0: its argsort (P)
 };
 
 // NumPy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
@@ -135,25 +139,151 @@ __device__ __forceinline__ double block_reduce(double v, bool is_max, double* sc
   return v;
 }
 
+// Bitonic sort of P = 2^m keys with an int payload (ascending by key).
+__device__ void bitonic_sort_kv(double* key, int* val, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const double x = key[lo], y = key[hi];
+        if ((x > y) == up) {
+          key[lo] = y; key[hi] = x;
+          const int v = val[lo]; val[lo] = val[hi]; val[hi] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ void bitonic_sort_k(double* key, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const double x = key[lo], y = key[hi];
+        if ((x > y) == up) { key[lo] = y; key[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// (k+1) smallest max-norm distances of point (xi, yi), found at sorted position q
+// of an array sorted by x (sx) with the other coordinate in the same order (yx):
+// scan outward in |x_i - x_j| order until that alone reaches the running (k+1)-th
+// distance.  Every j with |dx| < eps is visited, so the result equals the
+// brute-force order statistic.  Self is the 0 in top[0].
+template <int KP1>
+__device__ __forceinline__ double knn_scan(const double* __restrict__ sx,
+                                           const double* __restrict__ yx, int M, int q) {
+  const double xi = sx[q], yi = yx[q];
+  double top[KP1];
+  top[0] = 0.0;
+#pragma unroll
+  for (int s = 1; s < KP1; ++s) top[s] = INFINITY;
+  int l = q - 1, r = q + 1;
+  double dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY;      // = |x_i - x_l| exactly
+  double dr = r < M ? dsub(sx[r], xi) : INFINITY;
+  for (;;) {
+    const bool left = dl <= dr;
+    const double dx = left ? dl : dr;
+    if (!(dx < top[KP1 - 1])) break;
+    const int j = left ? l : r;
+    const double d = fmax(dx, fabs(dsub(yi, yx[j])));
+    if (d < top[KP1 - 1]) {
+#pragma unroll
+      for (int s = KP1 - 1; s > 0; --s) top[s] = d < top[s - 1] ? top[s - 1] : fmin(d, top[s]);
+      top[0] = fmin(d, top[0]);
+    }
+    if (left) { --l; dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY; }
+    else { ++r; dr = r < M ? dsub(sx[r], xi) : INFINITY; }
+  }
+  return top[KP1 - 1];
+}
+
+// Distance from sorted position q to its k-th nearest neighbour along one axis
+// (a lower bound of the max-norm k-NN radius).
+__device__ __forceinline__ double kth_gap_1d(const double* __restrict__ s, int M, int q, int k) {
+  int l = q - 1, r = q + 1;
+  double d = 0.0;
+  for (int c = 0; c < k; ++c) {
+    const double dl = l >= 0 ? dsub(s[q], s[l]) : INFINITY;
+    const double dr = r < M ? dsub(s[r], s[q]) : INFINITY;
+    if (dl <= dr) { d = dl; --l; } else { d = dr; ++r; }
+  }
+  return d;
+}
+
+__device__ __forceinline__ int lower_bound_lt(const double* s, int P, double x);
+__device__ __forceinline__ int upper_bound_le(const double* s, int P, double x);
+
+// Candidates a scan along an axis would visit at radius lb (points with |d| < lb).
+__device__ __forceinline__ int strip_count(const double* s, int P, double c, double lb) {
+  return lower_bound_lt(s, P, dadd(c, lb)) - upper_bound_le(s, P, dsub(c, lb));
+}
+
+// Reference mode prep: jitter + sort the fixed reference vector once per query.
+__global__ void ksg_prep_ref_kernel(const double* __restrict__ ref, const double* __restrict__ jit,
+                                    int M, int P, double* sa_out, int* perm_out) {
+  extern __shared__ __align__(16) double sm[];
+  double* key = sm;
+  int* val = reinterpret_cast<int*>(key + P);
+  double* scratch = reinterpret_cast<double*>(val + P + (P & 1));
+  double amin = INFINITY, amax = -INFINITY;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    amin = fmin(amin, ref[i]);
+    amax = fmax(amax, ref[i]);
+  }
+  amin = block_reduce(amin, false, scratch);
+  amax = block_reduce(amax, true, scratch);
+  const double sc = dmul(1e-10, dsub(amax, amin));
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    key[i] = i < M ? dadd(ref[i], dmul(jit[i], sc)) : INFINITY;
+    val[i] = i < M ? i : M;
+  }
+  __syncthreads();
+  bitonic_sort_kv(key, val, P);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    sa_out[i] = key[i];
+    perm_out[i] = val[i];
+  }
+}
+
 template <int KP1>
 __global__ void __launch_bounds__(kKsgThreads)
 ksg_kernel(const KsgArgs g) {
   extern __shared__ __align__(16) double sm[];
   const int M = g.M, P = g.P;
-  double* aj = sm;
-  double* bj = aj + M;
-  double* sa = bj + M;
-  double* sb = sa + P;
-  double* terms = sb + P;
-  double* scratch = terms + M;      // 32 doubles
+  double* sa = sm;                 // a' sorted ascending (P, +inf padded)
+  double* bsa = sa + P;            // b' in a'-order
+  double* sb = bsa + P;            // b' sorted ascending (P, +inf padded)
+  double* asb = sb + P;            // a' in b'-order
+  double* A0 = asb + P;            // a' in original order (M)
+  double* B0 = A0 + M;             // b' in original order (M)
+  double* terms = B0 + M;          // psi(n_x+1) + psi(n_y+1), original order (M)
+  double* scratch = terms + M;     // 32
+  int* pa = reinterpret_cast<int*>(scratch + 32);   // a'-sorted position -> original index
+  int* pb = pa + P;                                  // b'-sorted position -> original index
+  int* posb = pb + P;                                // original index -> b'-sorted position
   __shared__ int bad_flag;
+  const int k = KP1 - 1;
 
   for (int64_t p = blockIdx.x; p < g.n; p += gridDim.x) {
-    // ---- load (fp32 node values are exact in fp64) --------------------------
+    // ---- load (fp32 node values are exact in fp64) -----------------------------
+    if (g.mode == 0) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        sa[i] = g.sa_ref[i];
+        pa[i] = g.perm_ref[i];
+      }
+    }
     for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      double a, b;
+      double a = 0.0, b;
       if (g.mode == 0) {
-        a = g.ref[i];
         b = (double)__ldg(g.X + (int64_t)i * g.V + (g.v0 + p));
       } else if (g.mode == 1) {
         a = g.A[p * g.a_stride + i];
@@ -162,79 +292,75 @@ ksg_kernel(const KsgArgs g) {
         a = (double)__ldg(g.X + g.pa[p] * (int64_t)M + i);
         b = (double)__ldg(g.X + g.pb[p] * (int64_t)M + i);
       }
-      aj[i] = a;
-      bj[i] = b;
+      A0[i] = a;
+      B0[i] = b;
     }
     if (threadIdx.x == 0) bad_flag = 0;
     __syncthreads();
-    // ---- ptp + jitter ----------------------------------------------------------
-    double amin = INFINITY, amax = -INFINITY, bmin = INFINITY, bmax = -INFINITY;
+    // ---- ptp + jitter (measures.py:190-192) -------------------------------------
+    double bmin = INFINITY, bmax = -INFINITY, amin = INFINITY, amax = -INFINITY;
     for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      amin = fmin(amin, aj[i]); amax = fmax(amax, aj[i]);
-      bmin = fmin(bmin, bj[i]); bmax = fmax(bmax, bj[i]);
+      bmin = fmin(bmin, B0[i]); bmax = fmax(bmax, B0[i]);
+      if (g.mode != 0) { amin = fmin(amin, A0[i]); amax = fmax(amax, A0[i]); }
     }
-    amin = block_reduce(amin, false, scratch);
-    amax = block_reduce(amax, true, scratch);
     bmin = block_reduce(bmin, false, scratch);
     bmax = block_reduce(bmax, true, scratch);
-    const double sca = dmul(1e-10, dsub(amax, amin));
     const double scb = dmul(1e-10, dsub(bmax, bmin));
+    double sca = 0.0;
+    if (g.mode != 0) {
+      amin = block_reduce(amin, false, scratch);
+      amax = block_reduce(amax, true, scratch);
+      sca = dmul(1e-10, dsub(amax, amin));
+    }
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       if (i < M) {
-        const double r = g.jit[i];
-        const double x = dadd(aj[i], dmul(r, sca));
-        const double y = dadd(bj[i], dmul(r, scb));
-        aj[i] = x; bj[i] = y;
-        sa[i] = x; sb[i] = y;
+        const double y = dadd(B0[i], dmul(g.jit[i], scb));
+        B0[i] = y;
+        sb[i] = y;
+        pb[i] = i;
+        if (g.mode != 0) {
+          const double x = dadd(A0[i], dmul(g.jit[i], sca));
+          A0[i] = x;
+          sa[i] = x;
+          pa[i] = i;
+        }
       } else {
-        sa[i] = INFINITY; sb[i] = INFINITY;
+        sb[i] = INFINITY;
+        pb[i] = M;
+        if (g.mode != 0) { sa[i] = INFINITY; pa[i] = M; }
       }
     }
     __syncthreads();
-    bitonic_sort2(sa, sb, P);
-    // ---- k-NN in max-norm: (k+1) smallest incl. self --------------------------
-    for (int i0 = threadIdx.x; i0 < M; i0 += kKsgPts * blockDim.x) {
-      double xi[kKsgPts], yi[kKsgPts], top[kKsgPts][KP1];
-#pragma unroll
-      for (int q = 0; q < kKsgPts; ++q) {
-        const int i = i0 + q * blockDim.x;
-        xi[q] = i < M ? aj[i] : 0.0;
-        yi[q] = i < M ? bj[i] : 0.0;
-#pragma unroll
-        for (int s = 0; s < KP1; ++s) top[q][s] = INFINITY;
+    if (g.mode == 0)
+      for (int q = threadIdx.x; q < M; q += blockDim.x) A0[pa[q]] = sa[q];
+    if (g.mode != 0) bitonic_sort_kv(sa, pa, P);
+    bitonic_sort_kv(sb, pb, P);      // ends with __syncthreads
+    for (int q = threadIdx.x; q < P; q += blockDim.x) {
+      bsa[q] = q < M ? B0[pa[q]] : 0.0;
+      asb[q] = q < M ? A0[pb[q]] : 0.0;
+      if (q < M) posb[pb[q]] = q;
+    }
+    __syncthreads();
+    // ---- k-NN (exact, scanned along the sparser axis) + marginal counts ------------
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      const int i = pa[q];
+      const int qb = posb[i];
+      const double xi = sa[q], yi = bsa[q];
+      // lower bound of eps; scan the axis whose strip at that radius is thinner
+      const double lb = fmax(kth_gap_1d(sa, M, q, k), kth_gap_1d(sb, M, qb, k));
+      const bool along_b = strip_count(sb, P, yi, lb) < strip_count(sa, P, xi, lb);
+      const double eps = along_b ? knn_scan<KP1>(sb, asb, M, qb) : knn_scan<KP1>(sa, bsa, M, q);
+      const int nx = lower_bound_lt(sa, P, dadd(xi, eps)) - upper_bound_le(sa, P, dsub(xi, eps)) - 1;
+      const int ny = lower_bound_lt(sb, P, dadd(yi, eps)) - upper_bound_le(sb, P, dsub(yi, eps)) - 1;
+      if (g.counts) {
+        g.counts[(p * 2) * (int64_t)M + i] = nx;
+        g.counts[(p * 2 + 1) * (int64_t)M + i] = ny;
       }
-      for (int j = 0; j < M; ++j) {
-        const double xj = aj[j], yj = bj[j];
-#pragma unroll
-        for (int q = 0; q < kKsgPts; ++q) {
-          const double d = fmax(fabs(dsub(xi[q], xj)), fabs(dsub(yi[q], yj)));
-          if (d < top[q][KP1 - 1]) {
-#pragma unroll
-            for (int s = KP1 - 1; s > 0; --s)
-              top[q][s] = d < top[q][s - 1] ? top[q][s - 1] : fmin(d, top[q][s]);
-            top[q][0] = fmin(d, top[q][0]);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kKsgPts; ++q) {
-        const int i = i0 + q * blockDim.x;
-        if (i >= M) continue;
-        const double eps = top[q][KP1 - 1];
-        const int nx = lower_bound_lt(sa, P, dadd(xi[q], eps)) -
-                       upper_bound_le(sa, P, dsub(xi[q], eps)) - 1;
-        const int ny = lower_bound_lt(sb, P, dadd(yi[q], eps)) -
-                       upper_bound_le(sb, P, dsub(yi[q], eps)) - 1;
-        if (g.counts) {
-          g.counts[(p * 2) * (int64_t)M + i] = nx;
-          g.counts[(p * 2 + 1) * (int64_t)M + i] = ny;
-        }
-        if (nx < 0 || ny < 0) {
-          bad_flag = 1;
-          terms[i] = __longlong_as_double(0x7ff8000000000000ll);
-        } else {
-          terms[i] = dadd(g.psi[nx], g.psi[ny]);
-        }
+      if (nx < 0 || ny < 0) {
+        bad_flag = 1;
+        terms[i] = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        terms[i] = dadd(g.psi[nx], g.psi[ny]);
       }
     }
     __syncthreads();
@@ -249,7 +375,9 @@ ksg_kernel(const KsgArgs g) {
   }
 }
 
-size_t ksg_smem_bytes(int M, int P) { return sizeof(double) * (3 * (size_t)M + 2 * P + 32); }
+size_t ksg_smem_bytes(int M, int P) {
+  return sizeof(double) * (4 * (size_t)P + 3 * (size_t)M + 32) + sizeof(int) * 3 * (size_t)P;
+}
 
 template <int KP1>
 static int launch_ksg_t(const KsgArgs& g, cudaStream_t s) {
@@ -266,7 +394,31 @@ static int launch_ksg_t(const KsgArgs& g, cudaStream_t s) {
   return NDF_OK;
 }
 
+static int launch_ksg_body(KsgArgs g, cudaStream_t s);
+
 static int launch_ksg(KsgArgs g, cudaStream_t s) {
+  void* scratch = nullptr;
+  int st = NDF_OK;
+  if (g.mode == 0 && g.n > 0 && g.M >= 2 && g.M <= 4096) {
+    int P = 1;
+    while (P < g.M) P <<= 1;
+    NDF_CUDA_CHECK(cudaMallocAsync(&scratch, (size_t)P * (sizeof(double) + sizeof(int)), s));
+    g.sa_ref = reinterpret_cast<double*>(scratch);
+    g.perm_ref = reinterpret_cast<int*>(reinterpret_cast<double*>(scratch) + P);
+    const size_t smem = (size_t)P * (sizeof(double) + sizeof(int)) + 8 + 32 * sizeof(double);
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(ksg_prep_ref_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ksg_prep_ref_kernel<<<1, kKsgThreads, smem, s>>>(g.ref, g.jit, g.M, P,
+                                                     const_cast<double*>(g.sa_ref),
+                                                     const_cast<int*>(g.perm_ref));
+    NDF_LAUNCH_CHECK();
+  }
+  st = launch_ksg_body(g, s);
+  if (scratch) cudaFreeAsync(scratch, s);
+  return st;
+}
+
+static int launch_ksg_body(KsgArgs g, cudaStream_t s) {
   NDF_REQUIRE(g.M >= 2, NDF_ERR_PARAMETER, "KSG needs at least two samples");
   NDF_REQUIRE(g.k >= 1 && g.k <= g.M - 1, NDF_ERR_PARAMETER, "need 1 <= k <= N-1");
   NDF_REQUIRE(g.k <= 16, NDF_ERR_UNSUPPORTED, "GPU KSG supports k <= 16");
