@@ -45,6 +45,19 @@ PAPER_MS = 9.0          # PAPER.md:344/350, RTX 3090
 FLOP_PER_PAIR = 2 * (110 * 128 + 128 * 128 * 2 + 128)   # 93,952
 
 
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+SFU_OPS_PER_PAIR = 3 * 128      # one tanh.approx per hidden activation
+SFU_PER_CLK_SM = 16             # measured, tools/micro/mufu_rate.cu
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -316,6 +329,10 @@ def run_ours(args):
     if rank == 0:
         achieved_tflops = FLOP_PER_PAIR * (v1 - v0) / (kms * 1e-3) / 1e12
         peak = peaks.get("bf16_tflops", 1590.0)
+        traffic = load_traffic()
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        sm_hz = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        sfu_floor_ms = SFU_OPS_PER_PAIR * (v1 - v0) / (SFU_PER_CLK_SM * sm_count * sm_hz) * 1e3
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -330,7 +347,8 @@ def run_ours(args):
                          "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_tflops / peak, "peak_kind": f"{peak_kind} bf16 burst",
                          "kernel_ms": kms, "flop_per_launch": FLOP_PER_PAIR * (v1 - v0),
-                         "traffic": None},
+                         "traffic": traffic.get("query_tc_kernel"),
+                         "sfu_floor_ms": sfu_floor_ms, "sfu_frac": sfu_floor_ms / kms},
             "clocks": clocks,
             "gpu_launches": launches,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 24,
@@ -419,6 +437,7 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
         line["pearson_gemv"] = {
             "ms": gms, "bytes": gbytes, "achieved_gbs": gemv_gbs, "peak_gbs": hbm,
             "frac": gemv_gbs / hbm, "peak_kind": f"{peak_kind} hbm copy",
+            "traffic": load_traffic().get("gemv_kernel"),
             "zscore_prep_ms": zscore_ms, "members": M, "vertices": v1 - v0}
         line["ksg_mi"] = {"pairs_per_s": pairs_s, "unit": "pairs/s", "k": w2.ksg_k,
                           "members": ens2.member_count, "sample_pairs": k_v1 - k_v0,
