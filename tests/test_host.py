@@ -46,10 +46,27 @@ def test_status_mapping():
     N.check(0)
 
 
-def test_model_desc_layout():
+def test_model_desc_layout_matches_c_header(tmp_path):
+    """The ctypes mirror of ndf_model_desc has the C compiler's size and offsets."""
     import ctypes
-    # 5 + 3 + 9 int32 = 17 -> 68 bytes, padded to 72, then 4 pointers
-    assert ctypes.sizeof(N.ModelDesc) == 72 + 4 * 8
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    fields = [f for f, _ in N.ModelDesc._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"ndf_b200.h\"\n"
+                   "int main(void){printf(\"%zu\\n\", sizeof(ndf_model_desc));"
+                   + "".join(f'printf("%zu\\n", offsetof(ndf_model_desc, {f}));' for f in fields)
+                   + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                           check=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(N.ModelDesc)
+    for f, off in zip(fields, vals[1:]):
+        assert getattr(N.ModelDesc, f).offset == off, f
 
 
 def test_modelspec_baseline_shapes():
