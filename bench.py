@@ -442,6 +442,53 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
         line["ksg_mi"] = {"pairs_per_s": pairs_s, "unit": "pairs/s", "k": w2.ksg_k,
                           "members": ens2.member_count, "sample_pairs": k_v1 - k_v0,
                           "ms": kms, "full_field_s_extrapolated": V / pairs_s}
+    # ---- config 4: bulk estimator pairs (Pearson + KSG), sharded pair ranges ---------
+    n_pairs = args.c4_pairs
+    pa_all, pb_all = W.pair_list(W.CONFIGS[4], count=n_pairs, seed=2)
+    p0, p1 = min(n_pairs, rank * math.ceil(n_pairs / world)), min(n_pairs, (rank + 1) * math.ceil(n_pairs / world))
+    ens2.vertex_major()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    res = ndf.pair_estimators_device(ens2, "v", pa_all[p0:p1], pb_all[p0:p1], k=W.CONFIGS[4].ksg_k)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    c4_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    del res
+    ens2.drop_derived()
+    if rank == 0:
+        line["c4_bulk_pairs"] = {"pairs": n_pairs, "ms": c4_ms, "pairs_per_s": n_pairs / (c4_ms * 1e-3),
+                                 "estimators": ["pearson", "ksg_mi"], "k": W.CONFIGS[4].ksg_k,
+                                 "note": "seeded pair list (half uniform, half within +-16 cells), "
+                                         "subset of the 2^22 config-4 list; vertex-major copy built "
+                                         "before timing"}
+    # ---- config 3: 64-reference fp16 cube, both heads ---------------------------------
+    w3 = W.CONFIGS[3]
+    refs = W.reference_vertices(w3, count=64, seed=1)
+    pos = np.stack([np.array([2.0 * i / (n - 1) - 1.0 for i, n in
+                              zip((v % w3.dims[0], (v // w3.dims[0]) % w3.dims[1],
+                                   v // (w3.dims[0] * w3.dims[1])), w3.dims)]) for v in refs])
+    models = [W.build_model(w3, seed=0, grid_init=1e-4).with_precision(args.precision),
+              ndf.NdfModel.build(
+                  ndf.ModelSpec.baseline(w3.dims, w3.latent_factor, measure_kind="ksg_mi",
+                                         precision=args.precision), seed=1)]
+    cube = torch.empty((64, v1 - v0), dtype=torch.float16, device=dev)
+    c3 = []
+    for i in range(1 + max(1, args.steps // 5)):
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for m3 in models:
+            ndf.reconstruct_multi_device(m3, pos, ndf.ROLE_MU, w3.dims, v0, v1, out=cube)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            c3.append(t0.elapsed_time(t1))
+    c3_ms = max_over_ranks(statistics.mean(c3), world)
+    if rank == 0:
+        line["c3_multi_ref"] = {"refs": 64, "heads": 2, "pairs": 2 * 64 * V, "ms": c3_ms,
+                                "pairs_per_s": 2 * 64 * V / (c3_ms * 1e-3),
+                                "tflops": FLOP_PER_PAIR * 2 * 64 * V / (c3_ms * 1e-3) / 1e12,
+                                "output": "fp16 cube 64 x 1.76M per head"}
+    del cube
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
         procs = os.cpu_count() or 1
@@ -476,6 +523,7 @@ def main():
     ap.add_argument("--cpu-ksg-pairs", type=int, default=2048)
     ap.add_argument("--ksg-pairs", type=int, default=1 << 15)
     ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    ap.add_argument("--c4-pairs", type=int, default=1 << 16)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -26,6 +26,25 @@ int sm_count() {
   return cached;
 }
 
+// Stream-ordered scratch from the device's default memory pool.  The pool's release
+// threshold is raised once per device so synchronising callers (one query per
+// host round trip) do not pay an unmap / remap on every call.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (configured != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    configured = dev;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 }  // namespace ndf
 
 extern "C" int32_t ndf_abi_version(void) { return NDF_ABI_VERSION; }

@@ -49,6 +49,7 @@ void count_launch(int n = 1);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 
 // ---- exact IEEE fp64 helpers (no FMA contraction) ---------------------------
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }

@@ -402,7 +402,7 @@ static int launch_ksg(KsgArgs g, cudaStream_t s) {
   if (g.mode == 0 && g.n > 0 && g.M >= 2 && g.M <= 4096) {
     int P = 1;
     while (P < g.M) P <<= 1;
-    NDF_CUDA_CHECK(cudaMallocAsync(&scratch, (size_t)P * (sizeof(double) + sizeof(int)), s));
+    NDF_CUDA_CHECK(scratch_alloc(&scratch, (size_t)P * (sizeof(double) + sizeof(int)), s));
     g.sa_ref = reinterpret_cast<double*>(scratch);
     g.perm_ref = reinterpret_cast<int*>(reinterpret_cast<double*>(scratch) + P);
     const size_t smem = (size_t)P * (sizeof(double) + sizeof(int)) + 8 + 32 * sizeof(double);

@@ -281,6 +281,7 @@ struct TcArgs {
   int64_t ld_out;
   long long* trace;       // debug: per-phase clock64 stamps of CTA 0 (NULL = off)
   int stagger;            // cycles between warpgroup start times (de-phases the WGs)
+  int tokens;             // max warpgroups in an epilogue at once (0 = unlimited)
 };
 
 // debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
@@ -327,6 +328,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + nwg * kABytes);   // [0] weights, [1+w]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   float* eref_s = reinterpret_cast<float*>(bars + 16);      // single-ref grid: e_ref in SMEM
+  int* epi_tok = reinterpret_cast<int*>(bars + 64);          // epilogue admission counter
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -336,6 +338,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   const uint32_t tmem_cols = nwg > 2 ? 512 : (nwg == 2 ? 256 : 128);
 
   if (tid == 0) {
+    *epi_tok = 0;
     mbar_init(&bars[0], 1);
     for (int w = 0; w < nwg; ++w) mbar_init(&bars[1 + w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -467,6 +470,18 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
+        // Admission control: at most t.tokens warpgroups run the MUFU-bound epilogue at
+        // a time, which keeps the others in their encoder / MMA phases and stops the
+        // four warpgroups from phase-locking onto the same unit.
+        if (t.tokens > 0) {
+          if (wtid == 0) {
+            while (atomicAdd(epi_tok, 1) >= t.tokens) {
+              atomicSub(epi_tok, 1);
+              __nanosleep(32);
+            }
+          }
+          named_bar(bar_id, 128);
+        }
         NDF_TRACE(2 + 2 * l);
         const bool next_hidden = l + 1 < lay.H;
         const float4* nbias4 = reinterpret_cast<const float4*>(vecs + (l + 1) * kHid);
@@ -484,24 +499,29 @@ query_tc_kernel(const TcArgs t, const int nwg) {
             }
             tmem_st32(tmem_row + (uint32_t)c0, nb);
           }
+          float h[32];
+          if constexpr (SILU) {
+            // all 32 MUFU first (one in flight per scoreboard group), then the FMAs:
+            // x = z/2, silu(z) = x + x*tanh(x)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint32_t p[4];
+            for (int i = 0; i < 32; ++i) h[i] = tanh_fast(v[i]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float x0 = v[8 * j + 2 * q], x1 = v[8 * j + 2 * q + 1];
-              if constexpr (SILU)   // x = z/2: silu(z) = x + x*tanh(x)
-                p[q] = pack2<F16>(fmaf(x0, tanh_fast(x0), x0), fmaf(x1, tanh_fast(x1), x1));
-              else
-                p[q] = pack2<F16>(act_f32(a.m.activation, x0), act_f32(a.m.activation, x1));
-            }
-            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA), p[0], p[1], p[2], p[3]);
+            for (int i = 0; i < 32; ++i) h[i] = fmaf(v[i], h[i], v[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) h[i] = act_f32(a.m.activation, v[i]);
           }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA),
+                         pack2<F16>(h[8 * j], h[8 * j + 1]), pack2<F16>(h[8 * j + 2], h[8 * j + 3]),
+                         pack2<F16>(h[8 * j + 4], h[8 * j + 5]), pack2<F16>(h[8 * j + 6], h[8 * j + 7]));
         }
         if (next_hidden) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_proxy_async();
         tc_fence_before();
         named_bar(bar_id, 128);
+        if (t.tokens > 0 && wtid == 0) atomicSub(epi_tok, 1);
         NDF_TRACE(3 + 2 * l);
       }
       // ---- output layer (128 -> 1) as a 16-column MMA ---------------------------------
@@ -878,8 +898,11 @@ __global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, fl
     const int r = tid - naxis;
     const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
     float e[kE];
-    embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, grid, refs[3 * r], refs[3 * r + 1],
-                          refs[3 * r + 2], e);
+    // refs == nullptr: the single reference travels by value in the kernel arguments
+    const double rx = refs ? refs[3 * r] : a.ref[0];
+    const double ry = refs ? refs[3 * r + 1] : a.ref[1];
+    const double rz = refs ? refs[3 * r + 2] : a.ref[2];
+    embed_point_t<kL, kC>(a.g.rx, a.g.ry, a.g.rz, grid, rx, ry, rz, e);
     for (int i = 0; i < kERefStride; ++i) erefs[(size_t)r * kERefStride + i] = i < kE ? e[i] : 0.f;
   }
 }
@@ -1030,26 +1053,24 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
       stagger = e ? atoi(e) : 1500;
     }
     t.stagger = stagger;
+    static int tokens = -1;
+    if (tokens < 0) {
+      const char* e = getenv("NDF_TC_TOKENS");
+      tokens = e ? atoi(e) : 0;
+    }
+    t.tokens = tokens;
   }
   void* scratch = nullptr;
-  double* ref_host_dev = nullptr;
   if (a.mode == 0) {
     NDF_REQUIRE((int64_t)a.nx * a.ny * a.nz < (1LL << 32), NDF_ERR_UNSUPPORTED,
                 "tensor-core grid query supports < 2^32 vertices");
     const int naxis = a.nx + a.ny + a.nz;
     const size_t fbytes = (size_t)naxis * tc::kAxisRow * sizeof(float);
     const size_t ebytes = (size_t)n_ref * tc::kERefStride * sizeof(float);
-    const size_t rbytes = refs_dev ? 0 : 3 * sizeof(double);
-    NDF_CUDA_CHECK(cudaMallocAsync(&scratch, fbytes + ebytes + rbytes + 64, s));
+    NDF_CUDA_CHECK(scratch_alloc(&scratch, fbytes + ebytes + 64, s));
     t.ftab = reinterpret_cast<float*>(scratch);
     t.erefs = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(scratch) + fbytes);
     const double* refs = refs_dev;
-    if (!refs) {   // single reference: its coordinates travel as kernel arguments
-      ref_host_dev = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) + fbytes + ebytes);
-      NDF_CUDA_CHECK(cudaMemcpyAsync(ref_host_dev, a.ref, 3 * sizeof(double),
-                                     cudaMemcpyHostToDevice, s));
-      refs = ref_host_dev;
-    }
     const int threads = 128;
     tc::prep_kernel<<<(naxis + n_ref + threads - 1) / threads, threads, 0, s>>>(
         a, refs, n_ref, const_cast<float*>(t.ftab), const_cast<float*>(t.erefs));

@@ -73,8 +73,42 @@ def reconstruct_field(model: NdfModel, ref, role: str = ROLE_MU, dims=(64, 64, 6
     if batch_size < 1:
         raise ParameterError("batch_size must be >= 1")
     dims = _check_dims(dims)
-    out = reconstruct_field_device(model, ref, role, dims, clamp=clamp)
-    return FieldGrid(dims, to_host(out))
+    return FieldGrid(dims, _query_to_host(model, ref, role, dims, clamp))
+
+
+_COPY_STREAMS = {}
+
+
+def _query_to_host(model: NdfModel, ref, role, dims, clamp, chunks: int = 1) -> np.ndarray:
+    """Query + D2H into pinned memory.  With ``chunks`` > 1 the vertex range runs as
+    several launches while a side stream copies finished chunks (measured on B200:
+    the 7 MB copy takes 0.135 ms, less than the per-launch overhead chunking adds,
+    so one chunk is the default)."""
+    import torch
+    V = dims[0] * dims[1] * dims[2]
+    dev = model.device_state().device
+    if V < (1 << 18):
+        chunks = 1
+    out = torch.empty(V, dtype=torch.float32, device=dev)
+    host = torch.empty(V, dtype=torch.float32, pin_memory=True)
+    main = torch.cuda.current_stream(dev)
+    side = _COPY_STREAMS.get(str(dev))
+    if side is None:
+        side = _COPY_STREAMS[str(dev)] = torch.cuda.Stream(dev)
+    step = -(-V // chunks)
+    for c in range(chunks):
+        v0, v1 = c * step, min(V, (c + 1) * step)
+        if v0 >= v1:
+            break
+        reconstruct_field_device(model, ref, role, dims, v0, v1, out=out[v0:v1], clamp=clamp)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            host[v0:v1].copy_(out[v0:v1], non_blocking=True)
+    out.record_stream(side)
+    side.synchronize()
+    return host.numpy()
 
 
 def to_host(t) -> np.ndarray:
