@@ -116,24 +116,36 @@ __device__ __forceinline__ float act_f32(int kind, float x) {
   }
 }
 
-// Merged decoder-input element idx (model.py:279-286 + BASELINE's sum_absdiff).
+// Column of the tensor-core A operand that holds merged decoder input m.  For the
+// two-block merges (sum_absdiff, concat) the blocks are interleaved -- A[2i] from
+// e[i] of the first block, A[2i+1] of the second -- so each embedding element feeds
+// one adjacent pair of columns and dies at once (no long register live ranges in
+// the encoder); layer 0's weight rows are permuted identically at pack time.
+__host__ __device__ __forceinline__ int a_column(int merge, int m, int E) {
+  if (merge == NDF_MERGE_SUM_ABSDIFF || merge == NDF_MERGE_CONCAT)
+    return m < E ? 2 * m : 2 * (m - E) + 1;
+  return m;
+}
+
+// Value of A column c (model.py:279-286 + BASELINE's sum_absdiff), e_a = mu branch.
 // MERGE >= 0 fixes the mode at compile time; -1 reads it at run time.
 template <int MERGE, class FA, class FB>
-__device__ __forceinline__ float merged_value(int merge_rt, int idx, FA ea, FB eb) {
+__device__ __forceinline__ float merged_value(int merge_rt, int c, FA ea, FB eb) {
   const int merge = MERGE >= 0 ? MERGE : merge_rt;
-  if (idx < kE) {
-    const float a = ea(idx), b = eb(idx);
+  if (merge == NDF_MERGE_SUM_ABSDIFF || merge == NDF_MERGE_CONCAT) {
+    const int i = c >> 1;
+    if (i >= kE) return 0.0f;
+    const float a = ea(i), b = eb(i);
+    if (merge == NDF_MERGE_CONCAT) return (c & 1) ? b : a;
+    return (c & 1) ? fabsf(a - b) : a + b;
+  }
+  if (c < kE) {
+    const float a = ea(c), b = eb(c);
     switch (merge) {
       case NDF_MERGE_MULTIPLY: return a * b;
       case NDF_MERGE_ABSDIFF: return fabsf(a - b);
-      case NDF_MERGE_CONCAT: return a;
-      default: return a + b;          // add, sum_absdiff
+      default: return a + b;          // add
     }
-  }
-  if (idx < 2 * kE) {
-    const float a = ea(idx - kE), b = eb(idx - kE);
-    if (merge == NDF_MERGE_CONCAT) return b;
-    if (merge == NDF_MERGE_SUM_ABSDIFF) return fabsf(a - b);
   }
   return 0.0f;
 }
@@ -190,7 +202,28 @@ __device__ __forceinline__ void latent_f32(const float* __restrict__ grid, int r
 constexpr int kAxisRow = 16;
 static_assert(2 * kL + 4 == kAxisRow, "axis row layout");
 
-// Grid-mode embedding of node (ix, iy, iz): raw coords and the Fourier block come
+// Node (ix, iy, iz) of row `row` of `tile` (x fastest): one 32-bit division pair for
+// the tile's first vertex, then the row offset is carried along x.  Rows past the
+// end of the range are clamped to the last vertex (their results are discarded).
+__device__ __forceinline__ void tile_node(const QueryArgs& a, int64_t tile, int row, int& ix,
+                                          int& iy, int& iz) {
+  const int64_t n = a.v1 - a.v0;
+  const int64_t vloc = min(tile * kTileM + row, n - 1);
+  const int64_t vbase = tile * kTileM;
+  const uint32_t vb = (uint32_t)(a.v0 + vbase);
+  const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
+  iz = (int)(vb / nxy);
+  const uint32_t rem = vb - (uint32_t)iz * nxy;
+  iy = (int)(rem / (uint32_t)a.nx);
+  ix = (int)(rem - (uint32_t)iy * (uint32_t)a.nx) + (int)(vloc - vbase);
+  while (ix >= a.nx) {
+    ix -= a.nx;
+    if (++iy == a.ny) { iy = 0; ++iz; }
+  }
+}
+
+// Grid-mode embedding of node (ix, iy, iz) -- called by all 32 lanes of a warp
+// (invalid lanes pass a clamped node).  Raw coords and the Fourier block come
 // from the per-axis table; the latent cell is computed arithmetically
 // (u = i * (r-1)/(n-1) in fp32) so the latent gathers do not wait for the table
 // loads -- both go to L2 in one round trip (L1 is all SMEM here).
@@ -211,23 +244,72 @@ __device__ __forceinline__ void embed_grid_node(const QueryArgs& a, const float*
     tt[ax] = fminf(u - (float)i0[ax], 1.0f);
   }
   float acc[kC];
+  // Warp-cooperative latent gather: the 32 lanes are consecutive x nodes, normally of
+  // one (y, z) row, so they share the y/z cell and weights and touch only a few
+  // x cells.  Lane L pre-interpolates column xmin+L over (y, z) (4 rows) and every lane
+  // then lerps its two columns from registers via shuffles: ~6x fewer L2 requests.
+  const unsigned full = 0xffffffffu;
+  const int iy0 = __shfl_sync(full, i0[1], 0), iz0 = __shfl_sync(full, i0[2], 0);
+  const float ty0 = __shfl_sync(full, tt[1], 0), tz0 = __shfl_sync(full, tt[2], 0);
+  const int xmin = __reduce_min_sync(full, i0[0]);
+  const int xmax = __reduce_max_sync(full, i0[0]);
+  const bool coop = __all_sync(full, i0[1] == iy0 && i0[2] == iz0 && tt[1] == ty0 &&
+                                         tt[2] == tz0) && (xmax - xmin + 2 <= 32);
+  if (coop) {
+    const int lane = threadIdx.x & 31;
+    const int nc = xmax - xmin + 2;
+    float g[kC];
 #pragma unroll
-  for (int ch = 0; ch < kC; ++ch) acc[ch] = 0.0f;
+    for (int ch = 0; ch < kC; ++ch) g[ch] = 0.0f;
+    if (lane < nc) {
+      const int xl = xmin + lane;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
-    const float w = (dx ? tt[0] : 1.0f - tt[0]) * (dy ? tt[1] : 1.0f - tt[1]) *
-                    (dz ? tt[2] : 1.0f - tt[2]);
-    const int idx = (i0[0] + dx) + a.g.rx * ((i0[1] + dy) + a.g.ry * (i0[2] + dz));
-    const float4* row = reinterpret_cast<const float4*>(grid + (size_t)idx * kC);
+      for (int c = 0; c < 4; ++c) {
+        const int dy = c & 1, dz = c >> 1;
+        const float w = (dy ? ty0 : 1.0f - ty0) * (dz ? tz0 : 1.0f - tz0);
+        const int idx = xl + a.g.rx * ((iy0 + dy) + a.g.ry * (iz0 + dz));
+        const float4* row = reinterpret_cast<const float4*>(grid + (size_t)idx * kC);
 #pragma unroll
-    for (int q = 0; q < kC / 4; ++q) {
-      const float4 f = __ldg(row + q);
-      acc[4 * q + 0] = fmaf(w, f.x, acc[4 * q + 0]);
-      acc[4 * q + 1] = fmaf(w, f.y, acc[4 * q + 1]);
-      acc[4 * q + 2] = fmaf(w, f.z, acc[4 * q + 2]);
-      acc[4 * q + 3] = fmaf(w, f.w, acc[4 * q + 3]);
+        for (int q = 0; q < kC / 4; ++q) {
+          const float4 f = __ldg(row + q);
+          g[4 * q + 0] = fmaf(w, f.x, g[4 * q + 0]);
+          g[4 * q + 1] = fmaf(w, f.y, g[4 * q + 1]);
+          g[4 * q + 2] = fmaf(w, f.z, g[4 * q + 2]);
+          g[4 * q + 3] = fmaf(w, f.w, g[4 * q + 3]);
+        }
+      }
     }
+    const int src = i0[0] - xmin;
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) {
+      const float g0 = __shfl_sync(full, g[ch], src);
+      const float g1 = __shfl_sync(full, g[ch], src + 1);
+      acc[ch] = fmaf(tt[0], g1 - g0, g0);
+    }
+  } else {
+    // same arithmetic per lane (columns x0 and x0+1 over (y, z), then the x lerp), so
+    // a vertex's value does not depend on which path its warp took
+    float g0[kC], g1[kC];
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) { g0[ch] = 0.0f; g1[ch] = 0.0f; }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int dy = c & 1, dz = c >> 1;
+      const float w = (dy ? tt[1] : 1.0f - tt[1]) * (dz ? tt[2] : 1.0f - tt[2]);
+      const int idx = i0[0] + a.g.rx * ((i0[1] + dy) + a.g.ry * (i0[2] + dz));
+      const float4* r0 = reinterpret_cast<const float4*>(grid + (size_t)idx * kC);
+      const float4* r1 = reinterpret_cast<const float4*>(grid + (size_t)(idx + 1) * kC);
+#pragma unroll
+      for (int q = 0; q < kC / 4; ++q) {
+        const float4 f = __ldg(r0 + q), h = __ldg(r1 + q);
+        g0[4 * q + 0] = fmaf(w, f.x, g0[4 * q + 0]); g1[4 * q + 0] = fmaf(w, h.x, g1[4 * q + 0]);
+        g0[4 * q + 1] = fmaf(w, f.y, g0[4 * q + 1]); g1[4 * q + 1] = fmaf(w, h.y, g1[4 * q + 1]);
+        g0[4 * q + 2] = fmaf(w, f.z, g0[4 * q + 2]); g1[4 * q + 2] = fmaf(w, h.z, g1[4 * q + 2]);
+        g0[4 * q + 3] = fmaf(w, f.w, g0[4 * q + 3]); g1[4 * q + 3] = fmaf(w, h.w, g1[4 * q + 3]);
+      }
+    }
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) acc[ch] = fmaf(tt[0], g1[ch] - g0[ch], g0[ch]);
   }
   const int rows[3] = {ix, a.nx + iy, a.nx + a.ny + iz};
 #pragma unroll
@@ -286,6 +368,7 @@ struct TcArgs {
 
 // debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
 constexpr int kTraceTiles = 32, kTraceEvents = 12;
+constexpr int kTraceBase = 6 * kTraceTiles * kTraceEvents;   // + 16 chunk stamps
 #define NDF_TRACE_AT(slot_, ev)                                                          \
   do {                                                                                   \
     if (t.trace && blockIdx.x == 0 && wtid == 0 && (slot_) < kTraceTiles)                 \
@@ -406,20 +489,14 @@ query_tc_kernel(const TcArgs t, const int nwg) {
     const bool valid = vloc < n;
     // ---- K1: embed the query vertex once -----------------------------------------
     float eq[kE];
-    if (valid && KIND != kPoints) {
-      // vertex -> (ix, iy, iz): one 32-bit division pair for the tile's first vertex
-      // (warp-uniform), then carry the thread's offset along x (x fastest).
-      const uint32_t vb = (uint32_t)(a.v0 + tile * kTileM);
-      const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
-      int iz = (int)(vb / nxy);
-      const uint32_t rem = vb - (uint32_t)iz * nxy;
-      int iy = (int)(rem / (uint32_t)a.nx);
-      int ix = (int)(rem - (uint32_t)iy * (uint32_t)a.nx) + wtid;
-      while (ix >= a.nx) {
-        ix -= a.nx;
-        if (++iy == a.ny) { iy = 0; ++iz; }
+    if (KIND != kPoints) {
+      int ix, iy, iz;
+      tile_node(a, tile, wtid, ix, iy, iz);
+      embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);   // all lanes (shuffles)
+      if (!valid) {
+#pragma unroll
+        for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
       }
-      embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);
       NDF_TRACE(8);
     } else if (valid) {
       embed_point_tc(a, a.m.grid_nu, a.p_nu + 3 * (a.v0 + vloc), eq);
@@ -488,7 +565,12 @@ query_tc_kernel(const TcArgs t, const int nwg) {
 #pragma unroll 1
         for (int c0 = 0; c0 < kHid; c0 += 32) {
           float v[32];
+#define NDF_CHUNK_TRACE(e)                                                                   \
+  if (t.trace && blockIdx.x == 0 && wg == 0 && wtid == 0 && tcount == 3 && l == 1)          \
+    t.trace[kTraceBase + (c0 >> 5) * 4 + (e)] = clock64();
+          NDF_CHUNK_TRACE(0);
           tmem_ld32(tmem_row + (uint32_t)c0, v);          // z (or z/2 for SiLU) incl. bias
+          NDF_CHUNK_TRACE(1);
           if (next_hidden) {                               // next layer's bias -> same columns
             uint32_t nb[32];
 #pragma unroll
@@ -499,6 +581,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
             }
             tmem_st32(tmem_row + (uint32_t)c0, nb);
           }
+          NDF_CHUNK_TRACE(2);
           float h[32];
           if constexpr (SILU) {
             // all 32 MUFU first (one in flight per scoreboard group), then the FMAs:
@@ -516,6 +599,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
             st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA),
                          pack2<F16>(h[8 * j], h[8 * j + 1]), pack2<F16>(h[8 * j + 2], h[8 * j + 3]),
                          pack2<F16>(h[8 * j + 4], h[8 * j + 5]), pack2<F16>(h[8 * j + 6], h[8 * j + 7]));
+          NDF_CHUNK_TRACE(3);
         }
         if (next_hidden) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_proxy_async();
@@ -555,20 +639,17 @@ query_tc_kernel(const TcArgs t, const int nwg) {
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised schedule (NDF_TC_SCHEDULE=ws).  Four TMEM-accumulator / A-buffer slots.
-//   WG0, WG1 -- epilogue warpgroups: drain accumulators (tcgen05.ld, software-
-//               pipelined one 32-column chunk ahead), bias + activation, write the
-//               next A operand, issue the next MMA.  Each owns two slots and
-//               alternates between them with slot B running two stages behind slot
-//               A, so (i) its epilogue on one slot hides the MMA of the other and
-//               (ii) the two slots are released at different times.
-//   WG2, WG3 -- producer warpgroups: embed the next query tile and pack its merged
-//               16-bit layer-0 rows in registers *before* the slot frees, then only
-//               store them (14 x 16 B per row) and issue the layer-0 MMA.
-// Slot s is shared by epilogue WG (s & 1) and producer WG 2 + (s & 1); the pair
-// walks the deterministic item sequence j = tile_k * n_ref + r, item j in slot
-// pair[j & 1].  Synchronisation is mbarrier-only: acc_full[s] (tcgen05.commit after
-// each MMA stage) and slot_free[s] (epilogue WG after reading the output column).
+// Warp-specialised schedule (NDF_TC_SCHEDULE=ws; single-reference grid queries).
+//   WG0..WG3 -- epilogue warpgroups, one TMEM-accumulator / A-buffer slot each:
+//               drain the accumulator (tcgen05.ld pipelined one 32-column chunk
+//               ahead), bias + activation, write the next A operand, issue the next
+//               MMA, and finally read the output column and release the slot.
+//   WG4, WG5 -- producer warpgroups: embed the next query tile and pack its merged
+//               16-bit layer-0 rows in registers *before* the slot is released, then
+//               only store them (14 x 16 B per row) and issue the layer-0 MMA, so
+//               the L2-latency-bound encoder never sits on the epilogue warps' path.
+// Synchronisation is mbarrier-only: acc_full[s] (tcgen05.commit after every MMA
+// stage) and slot_free[s] (epilogue WG after reading the output column).
 constexpr int kSlots = 4;
 constexpr int kKinMax = 128;
 
@@ -627,7 +708,7 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 
 template <bool F16, bool SILU, int KIND>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(768, 1)
 query_ws_kernel(const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const QueryArgs& a = t.q;
@@ -660,7 +741,7 @@ query_ws_kernel(const TcArgs t) {
                      smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (KIND == kGridSingle && tid < kERefStride) eref_s[tid] = t.erefs[tid];
+  if (tid < kERefStride) eref_s[tid] = t.erefs[tid];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -682,182 +763,138 @@ query_ws_kernel(const TcArgs t) {
 
   const int64_t n = a.v1 - a.v0;
   const int64_t n_tiles = (n + kTileM - 1) / kTileM;
-  const int n_ref = KIND == kGridMulti ? t.n_ref : 1;
-  const int pairid = wg & 1;                               // slot pair {pairid, pairid + 2}
-  const int pair_slots[2] = {pairid, pairid + 2};
-  const int64_t tile_first = (int64_t)blockIdx.x * 2 + pairid;
-  const int64_t tile_stride = (int64_t)gridDim.x * 2;
-  const int64_t my_tiles =
-      tile_first < n_tiles ? (n_tiles - tile_first + tile_stride - 1) / tile_stride : 0;
-  const int64_t n_items = my_tiles * n_ref;
-  const int bar_id = 1 + wg;
+  const int64_t tile_stride = (int64_t)gridDim.x * kSlots;
+  auto slot_tiles = [&](int s) -> int64_t {
+    const int64_t first = (int64_t)blockIdx.x * kSlots + s;
+    return first < n_tiles ? (n_tiles - first + tile_stride - 1) / tile_stride : 0;
+  };
   const float* grid_q = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
+  const int bar_id = 1 + wg;
 
-  if (wg >= 2) {
-    // ======================= producer warpgroup ==================================
+  if (wg >= kSlots) {
+    // ======================= producer warpgroups (WG4, WG5) =========================
+    // WG4 fills slots 0 and 2, WG5 slots 1 and 3, alternating; the next tile's merged
+    // 16-bit row is packed in registers before the slot is released.
+    const int pslots[2] = {wg - kSlots, wg - kSlots + 2};
+    const int64_t cnt[2] = {slot_tiles(pslots[0]), slot_tiles(pslots[1])};
     const float lscale[3] = {a.nx > 1 ? (float)(a.g.rx - 1) / (float)(a.nx - 1) : 0.0f,
                              a.ny > 1 ? (float)(a.g.ry - 1) / (float)(a.ny - 1) : 0.0f,
                              a.nz > 1 ? (float)(a.g.rz - 1) / (float)(a.nz - 1) : 0.0f};
     uint32_t free_ph[2] = {0u, 0u};
-    float eq[kE];
     bool weights_ready = false;
-    for (int64_t j = 0; j < n_items; ++j) {
-      const int64_t k = j / n_ref;
-      const int r = (int)(j - k * n_ref);
-      const int si = (int)(j & 1);
-      const int s = pair_slots[si];
-      const int64_t tile = tile_first + k * tile_stride;
-      const int64_t vloc = tile * kTileM + wtid;
-      const bool valid = vloc < n;
-      NDF_TRACE_AT((int)j, 0);
-      if (r == 0) {                                   // new tile: embed the query vertex
-        if (valid && KIND != kPoints) {
-          const uint32_t vb = (uint32_t)(a.v0 + tile * kTileM);
-          const uint32_t nxy = (uint32_t)a.nx * (uint32_t)a.ny;
-          int iz = (int)(vb / nxy);
-          const uint32_t rem = vb - (uint32_t)iz * nxy;
-          int iy = (int)(rem / (uint32_t)a.nx);
-          int ix = (int)(rem - (uint32_t)iy * (uint32_t)a.nx) + wtid;
-          while (ix >= a.nx) {
-            ix -= a.nx;
-            if (++iy == a.ny) { iy = 0; ++iz; }
-          }
-          embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);
-        } else if (valid) {
-          embed_point_tc(a, a.m.grid_nu, a.p_nu + 3 * (a.v0 + vloc), eq);
-        } else {
-#pragma unroll
-          for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
-        }
-      }
-      // merged layer-0 row, packed to 16 bit, ready before the slot frees
-      uint32_t pk[kKinMax / 2];
-      auto fq = [&](int i) { return eq[i]; };
-      if constexpr (KIND != kPoints) {
-        const float* er = t.erefs + (size_t)r * kERefStride;
-        auto fr = [&](int i) { return KIND == kGridSingle ? eref_s[i] : __ldg(er + i); };
-        if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)
-          pack_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(0, fr, fq, lay.kin, pk);
-        else if (a.ref_is_mu)
-          pack_input_row<F16, -1>(a.m.merge, fr, fq, lay.kin, pk);
-        else
-          pack_input_row<F16, -1>(a.m.merge, fq, fr, lay.kin, pk);
-      } else {
-        float em[kE];
-        if (valid) {
-          const int64_t im = a.n_mu == 1 ? 0 : a.v0 + vloc;
-          embed_point_tc(a, a.m.grid_mu, a.p_mu + 3 * im, em);
-        } else {
-#pragma unroll
-          for (int i = 0; i < kE; ++i) em[i] = 0.0f;
-        }
-        auto fm = [&](int i) { return em[i]; };
-        pack_input_row<F16, -1>(a.m.merge, fm, fq, lay.kin, pk);
-      }
-      NDF_TRACE_AT((int)j, 1);
-      if (!weights_ready) {
-        mbar_wait(wbar, 0);
-        weights_ready = true;
-      }
-      if (j >= 2) {                                   // slot must be drained first
-        mbar_wait(&slot_free[s], free_ph[si]);
-        free_ph[si] ^= 1u;
-      }
-      NDF_TRACE_AT((int)j, 2);
-      const uint32_t a_addr = smem_u32(abufs + s * kABytes);
-#pragma unroll
-      for (int kg = 0; kg < kKinMax / 8; ++kg)
-        if (8 * kg < lay.kin)
-          st_shared_v4(a_addr + canon_off(wtid, 8 * kg, kSboA), pk[4 * kg], pk[4 * kg + 1],
-                       pk[4 * kg + 2], pk[4 * kg + 3]);
-      fence_proxy_async();
-      tc_fence_before();
-      named_bar(bar_id, 128);
-      if (wtid == 0)
-        issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr, lay.kin, sbo_w0, idesc,
-                    &acc_full[s], 0u);
-      NDF_TRACE_AT((int)j, 3);
-    }
-  } else {
-    // ======================= epilogue warpgroup ==================================
-    mbar_wait(wbar, 0);
-    const float bias_out = vecs[lay.H * kHid];
-    const int n_st = lay.H + 1;                  // stages per item: H hidden + output
-    uint32_t acc_ph[2] = {0u, 0u};
-    int64_t item[2] = {0, 1};                    // current item of each slot
-    int stage[2] = {0, -2};                      // slot B runs two stages behind slot A
-    for (;;) {
-      bool any = false;
+    const int64_t rounds = cnt[0] > cnt[1] ? cnt[0] : cnt[1];
+    for (int64_t kk = 0; kk < rounds; ++kk) {
       for (int si = 0; si < 2; ++si) {
-        if (stage[si] < 0) { ++stage[si]; any = true; continue; }   // start-up skew
-        const int64_t j = item[si];
-        if (j >= n_items) continue;
-        any = true;
-        const int st = stage[si];
-        const int s = pair_slots[si];
-        const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(s * kHid);
-        const uint32_t a_addr = smem_u32(abufs + s * kABytes);
-        mbar_wait(&acc_full[s], acc_ph[si]);
-        acc_ph[si] ^= 1u;
-        tc_fence_after();
-        NDF_TRACE_AT((int)(j >> 1), si * 5 + min(st, 4));
-        if (st < lay.H) {
-          // ---- hidden layer st: drain, bias + activation, write next A, next MMA ----
-          const float4* b4 = reinterpret_cast<const float4*>(vecs + st * kHid);
-          float va[32], vb[32];
-          tmem_ld32_nowait(tmem_row, va);
-          tmem_wait_ld();
-          tmem_ld32_nowait(tmem_row + 32u, vb);
-          epilogue_chunk<F16, SILU>(va, b4, 0, a.m.activation, a_addr, wtid);
-          tmem_wait_ld();
-          tmem_ld32_nowait(tmem_row + 64u, va);
-          epilogue_chunk<F16, SILU>(vb, b4, 32, a.m.activation, a_addr, wtid);
-          tmem_wait_ld();
-          tmem_ld32_nowait(tmem_row + 96u, vb);
-          epilogue_chunk<F16, SILU>(va, b4, 64, a.m.activation, a_addr, wtid);
-          tmem_wait_ld();
-          epilogue_chunk<F16, SILU>(vb, b4, 96, a.m.activation, a_addr, wtid);
-          fence_proxy_async();
-          tc_fence_before();
-          named_bar(bar_id, 128);
-          if (wtid == 0) {
-            if (st + 1 < lay.H)
-              issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr,
-                          w_addr + lay.w0_bytes + st * lay.wh_bytes, kHid, kSboA, idesc,
-                          &acc_full[s], 0u);
-            else
-              issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr + lay.wout_off,
-                          kHid, kSboA, idesc_out, &acc_full[s], 0u);
-          }
-          stage[si] = st + 1;
-        } else {
-          // ---- output column: head, store, release the slot ---------------------------
-          uint32_t zr;
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                       : "=r"(zr) : "r"(tmem_row));
-          tmem_wait_ld();
-          tc_fence_before();
-          const int64_t k = j / n_ref;
-          const int r = (int)(j - k * n_ref);
-          const int64_t vloc = (tile_first + k * tile_stride) * kTileM + wtid;
-          if (vloc < n) {
-            const float z = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
-            if (t.out16) {
-              const __half hz = __float2half_rn(z);
-              t.out16[(size_t)r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&hz);
-            } else {
-              a.out[vloc] = z;
+        if (kk >= cnt[si]) continue;
+        const int s = pslots[si];
+        const int64_t tile = (int64_t)blockIdx.x * kSlots + s + kk * tile_stride;
+        const int64_t vloc = tile * kTileM + wtid;
+        const int tslot = (int)(kk * 2 + si);
+        NDF_TRACE_AT(tslot, 0);
+        uint32_t pk[kKinMax / 2];
+        {
+          float eq[kE];
+          {
+            int ix, iy, iz;
+            tile_node(a, tile, wtid, ix, iy, iz);
+            embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);   // all lanes
+            if (vloc >= n) {
+#pragma unroll
+              for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
             }
           }
-          named_bar(bar_id, 128);
-          if (wtid == 0) mbar_arrive(&slot_free[s]);
-          NDF_TRACE_AT((int)(j >> 1), 10 + si);
-          item[si] = j + 2;
-          stage[si] = 0;
+          auto fq = [&](int i) { return eq[i]; };
+          auto fr = [&](int i) { return eref_s[i]; };
+          if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)
+            pack_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(0, fr, fq, lay.kin, pk);
+          else if (a.ref_is_mu)
+            pack_input_row<F16, -1>(a.m.merge, fr, fq, lay.kin, pk);
+          else
+            pack_input_row<F16, -1>(a.m.merge, fq, fr, lay.kin, pk);
         }
-        (void)n_st;
+        NDF_TRACE_AT(tslot, 1);
+        if (!weights_ready) {
+          mbar_wait(wbar, 0);
+          weights_ready = true;
+        }
+        if (kk >= 1) {                               // slot must be drained first
+          mbar_wait(&slot_free[s], free_ph[si]);
+          free_ph[si] ^= 1u;
+        }
+        NDF_TRACE_AT(tslot, 2);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+#pragma unroll
+        for (int kg = 0; kg < kKinMax / 8; ++kg)
+          if (8 * kg < lay.kin)
+            st_shared_v4(a_addr + canon_off(wtid, 8 * kg, kSboA), pk[4 * kg], pk[4 * kg + 1],
+                         pk[4 * kg + 2], pk[4 * kg + 3]);
+        fence_proxy_async();
+        tc_fence_before();
+        named_bar(bar_id, 128);
+        if (wtid == 0)
+          issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr, lay.kin, sbo_w0, idesc,
+                      &acc_full[s], 0u);
+        NDF_TRACE_AT(tslot, 3);
       }
-      if (!any) break;
+    }
+  } else {
+    // ======================= epilogue warpgroups (WG0..WG3, one slot each) ==========
+    const int s = wg;
+    const int64_t cnt = slot_tiles(s);
+    mbar_wait(wbar, 0);
+    const float bias_out = vecs[lay.H * kHid];
+    const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(s * kHid);
+    const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+    uint32_t acc_ph = 0u;
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+      for (int st = 0; st < lay.H; ++st) {
+        mbar_wait(&acc_full[s], acc_ph);
+        acc_ph ^= 1u;
+        tc_fence_after();
+        NDF_TRACE_AT((int)kk, 2 * st);
+        // ---- hidden layer st: drain (pipelined tcgen05.ld), bias + act, next A --------
+        const float4* b4 = reinterpret_cast<const float4*>(vecs + st * kHid);
+        float va[32], vb[32];
+        tmem_ld32_nowait(tmem_row, va);
+        tmem_wait_ld();
+        tmem_ld32_nowait(tmem_row + 32u, vb);
+        epilogue_chunk<F16, SILU>(va, b4, 0, a.m.activation, a_addr, wtid);
+        tmem_wait_ld();
+        tmem_ld32_nowait(tmem_row + 64u, va);
+        epilogue_chunk<F16, SILU>(vb, b4, 32, a.m.activation, a_addr, wtid);
+        tmem_wait_ld();
+        tmem_ld32_nowait(tmem_row + 96u, vb);
+        epilogue_chunk<F16, SILU>(va, b4, 64, a.m.activation, a_addr, wtid);
+        tmem_wait_ld();
+        epilogue_chunk<F16, SILU>(vb, b4, 96, a.m.activation, a_addr, wtid);
+        fence_proxy_async();
+        tc_fence_before();
+        named_bar(bar_id, 128);
+        NDF_TRACE_AT((int)kk, 2 * st + 1);
+        if (wtid == 0) {
+          if (st + 1 < lay.H)
+            issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr,
+                        w_addr + lay.w0_bytes + st * lay.wh_bytes, kHid, kSboA, idesc,
+                        &acc_full[s], 0u);
+          else
+            issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr + lay.wout_off, kHid,
+                        kSboA, idesc_out, &acc_full[s], 0u);
+        }
+      }
+      // ---- output column: head, store, release the slot -------------------------------
+      mbar_wait(&acc_full[s], acc_ph);
+      acc_ph ^= 1u;
+      tc_fence_after();
+      NDF_TRACE_AT((int)kk, 6);
+      uint32_t zr;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(zr) : "r"(tmem_row));
+      tmem_wait_ld();
+      tc_fence_before();
+      const int64_t vloc = ((int64_t)blockIdx.x * kSlots + s + kk * tile_stride) * kTileM + wtid;
+      if (vloc < n) a.out[vloc] = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
+      named_bar(bar_id, 128);
+      if (wtid == 0) mbar_arrive(&slot_free[s]);
     }
   }
   tc_fence_before();
@@ -941,7 +978,8 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
       uint8_t* dst = blob + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
       for (int64_t e = gtid; e < (int64_t)K * N; e += gsz) {
         const int k = (int)(e / N), nn = (int)(e % N);
-        store16(dst + canon_off(nn, k, sbo), hs * W[e], f16);
+        const int kc = l == 0 ? a_column(m.merge, k, kE) : k;   // layer-0 rows follow the A layout
+        store16(dst + canon_off(nn, kc, sbo), hs * W[e], f16);
       }
       for (int64_t e = gtid; e < N; e += gsz) vecs[l * kHid + e] = hs * b[e];
     } else {
@@ -981,23 +1019,24 @@ static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  // Schedule: "classic" (default; 4 symmetric warpgroups, one slot each) or "ws"
-  // (warp-specialised producer / epilogue warpgroups -- currently slower: the
-  // epilogue warps are MUFU-latency bound with only two per SM sub-partition).
+  // Schedule for single-reference grid queries: "ws" (default; 4 epilogue + 2
+  // producer warpgroups) or "classic" (4 symmetric warpgroups doing everything;
+  // also used for points and multi-reference queries).  Measured on B200 (c1):
+  // ws 0.328 ms, classic 0.375 ms per query.
   static int classic = -1;
   if (classic < 0) {
     const char* e = getenv("NDF_TC_SCHEDULE");
-    classic = (e && e[0] == 'w') ? 0 : 1;
+    classic = (e && e[0] == 'c') ? 1 : 0;
   }
-  if (classic || nwg != 4) {
+  if (classic || nwg != 4 || KIND != tc::kGridSingle) {
     tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
   } else {
-    // warp-specialised: one CTA covers 2 slot pairs; grid from the tile count
+    // warp-specialised: 4 epilogue + 2 producer warpgroups per CTA, one CTA per SM
     const int64_t n = t.q.v1 - t.q.v0;
     const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
     const unsigned g2 = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tiles + 3) / 4, sm_count()));
-    tc::query_ws_kernel<F16, SILU, KIND><<<g2, 512, smem, s>>>(t);
+    tc::query_ws_kernel<F16, SILU, KIND><<<g2, 768, smem, s>>>(t);
   }
   NDF_LAUNCH_CHECK();
   return NDF_OK;
@@ -1089,7 +1128,7 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) { return run_tc(a, nullp
 using namespace ndf;
 
 // Debug only (not part of the C-ABI header): subsequent tensor-core queries record
-// CTA 0's per-phase clock64() stamps into buf[4 * 32 * 12] (NULL disables).
+// CTA 0's per-phase clock64() stamps into buf[6 * 32 * 12 + 16] (NULL disables).
 extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 
 extern "C" size_t ndf_tc_blob_bytes(const ndf_model_desc* m) {

@@ -30,14 +30,19 @@ def main():
     lib = N.load_library()
     fn = lib.ndf_debug_tc_trace
     fn.argtypes = [ctypes.c_void_p]
-    buf = torch.zeros(4 * 32 * 12, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(6 * 32 * 12 + 16, dtype=torch.int64, device="cuda")
     for _ in range(3):
         ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
     fn(ctypes.c_void_p(buf.data_ptr()))
     ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
     torch.cuda.synchronize()
     fn(ctypes.c_void_p(0))
-    t = buf.cpu().numpy().reshape(4, 32, 12).astype(np.int64)
+    allb = buf.cpu().numpy().astype(np.int64)
+    ch = allb[6 * 32 * 12:].reshape(4, 4)
+    print("epilogue chunks (WG0 warp0, tile 3, layer 1): start, ld done, bias st done, end")
+    for c in range(4):
+        print("  chunk", c, ch[c] - ch[0, 0])
+    t = allb[:6 * 32 * 12].reshape(6, 32, 12)[:4]
     t0 = t[:, 0, 0].min()
     names = {0: "start", 8: "emb", 9: "bias", 11: "merge", 1: "A0", 2: "mma0", 3: "epi0",
              4: "mma1", 5: "epi1", 6: "mma2", 7: "epi2", 10: "out"}
