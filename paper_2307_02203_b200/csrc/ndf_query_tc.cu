@@ -116,14 +116,48 @@ __device__ __forceinline__ float act_f32(int kind, float x) {
   }
 }
 
-// Column of the tensor-core A operand that holds merged decoder input m.  For the
-// two-block merges (sum_absdiff, concat) the blocks are interleaved -- A[2i] from
-// e[i] of the first block, A[2i+1] of the second -- so each embedding element feeds
-// one adjacent pair of columns and dies at once (no long register live ranges in
-// the encoder); layer 0's weight rows are permuted identically at pack time.
+// Layer-0 A operand layout for the two-block merges (sum_absdiff, concat): the
+// blocks are interleaved -- 32-bit word w holds the 16-bit pair (first block,
+// second block) of ONE embedding feature -- and the words are grouped by which
+// grid axis the feature depends on, in 16-byte (4-word) groups:
+//   words  0..11  (sin, cos) of octaves 0..5 along x               groups 0-2
+//   words 12..35  (sin, cos) of octaves 0..5 along y, z (octave-major) groups 3-8
+//   words 36..51  latent channels 0..15                             groups 9-12
+//   words 52..54  raw x, y, z;  word 55 zero padding (K = 112)      group 13
+// For a grid query the Fourier-x groups depend only on the vertex column ix and
+// the Fourier-yz groups only on its row (iy, iz): they come pre-merged from small
+// per-query tables (prep_ws_merge_kernel) straight into the A buffer by cp.async, and
+// only the latent and raw words pass through registers.  Layer 0's weight rows
+// are permuted identically at pack time.
+constexpr int kWordFx = 0, kWordFyz = 12, kWordLat = 36, kWordRaw = 52;
+constexpr int kXTabWords = 16;    // per ix: Fourier-x words 0..11, raw-x word at 12
+constexpr int kYZTabWords = 32;   // per (iy, iz): Fourier-yz words 0..23, raw y, z at 24, 25
+
+// embedding feature (model.py:169-177 order: raw 3 | Fourier 6L | latent C) -> word
+__host__ __device__ __forceinline__ int word_of_feature(int f) {
+  if (f < 3) return kWordRaw + f;
+  if (f < 3 + 6 * kL) {
+    const int j = f - 3, i = j / 6, ax = (j % 6) >> 1, sc = j & 1;
+    return ax == 0 ? kWordFx + 2 * i + sc : kWordFyz + 4 * i + 2 * (ax - 1) + sc;
+  }
+  return kWordLat + (f - 3 - 6 * kL);
+}
+// inverse of word_of_feature; -1 for the padding word
+__host__ __device__ __forceinline__ int feature_of_word(int w) {
+  if (w < kWordFyz) return 3 + 6 * (w >> 1) + (w & 1);
+  if (w < kWordLat) {
+    const int j = w - kWordFyz, i = j >> 2, ax = 1 + ((j >> 1) & 1), sc = j & 1;
+    return 3 + 6 * i + 2 * ax + sc;
+  }
+  if (w < kWordRaw) return 3 + 6 * kL + (w - kWordLat);
+  return w < kWordRaw + 3 ? w - kWordRaw : -1;
+}
+
+// Column of the tensor-core A operand that holds merged decoder input m (row m of
+// W0).  Single-block merges keep the natural order.
 __host__ __device__ __forceinline__ int a_column(int merge, int m, int E) {
   if (merge == NDF_MERGE_SUM_ABSDIFF || merge == NDF_MERGE_CONCAT)
-    return m < E ? 2 * m : 2 * (m - E) + 1;
+    return m < E ? 2 * word_of_feature(m) : 2 * word_of_feature(m - E) + 1;
   return m;
 }
 
@@ -133,8 +167,8 @@ template <int MERGE, class FA, class FB>
 __device__ __forceinline__ float merged_value(int merge_rt, int c, FA ea, FB eb) {
   const int merge = MERGE >= 0 ? MERGE : merge_rt;
   if (merge == NDF_MERGE_SUM_ABSDIFF || merge == NDF_MERGE_CONCAT) {
-    const int i = c >> 1;
-    if (i >= kE) return 0.0f;
+    const int i = feature_of_word(c >> 1);
+    if (i < 0) return 0.0f;
     const float a = ea(i), b = eb(i);
     if (merge == NDF_MERGE_CONCAT) return (c & 1) ? b : a;
     return (c & 1) ? fabsf(a - b) : a + b;
@@ -331,6 +365,79 @@ __device__ __forceinline__ void embed_grid_node(const QueryArgs& a, const float*
   for (int ch = 0; ch < kC; ++ch) e[3 + 6 * kL + ch] = acc[ch];
 }
 
+// Arithmetic latent cell of node i on an n-node axis with r latent nodes: node i sits
+// at u = i*(r-1)/(n-1), a single-node axis at the domain centre u = (r-1)/2
+// (measures.py:245-247); fp32, as embed_grid_node.
+__device__ __forceinline__ void latent_cell(int i, int n, int r, int& i0, float& t) {
+  const float ls = n > 1 ? (float)(r - 1) / (float)(n - 1) : 0.0f;
+  const float u = n > 1 ? (float)i * ls : 0.5f * (float)(r - 1);
+  i0 = min((int)u, r - 2);
+  t = fminf(u - (float)i0, 1.0f);
+}
+
+// Latent channels of grid node (ix, iy, iz) from the per-query table that
+// prep_ws_feat_kernel has already interpolated along z: lerp in y, then in x.
+// Called by all 32 lanes; lanes of one (y, z) row share the row's few x cells
+// through shuffles (each lane loads one x cell of the two y rows).
+__device__ __forceinline__ void latent_yx_lerp(const float* __restrict__ lz, const QueryArgs& a,
+                                               int ix, int iy, int iz, float* acc) {
+  int x0, y0;
+  float tx, ty;
+  latent_cell(ix, a.nx, a.g.rx, x0, tx);
+  latent_cell(iy, a.ny, a.g.ry, y0, ty);
+  const unsigned full = 0xffffffffu;
+  const int yz = iy + a.ny * iz;
+  const int yz0 = __shfl_sync(full, yz, 0);
+  const int xmin = __reduce_min_sync(full, x0);
+  const int xmax = __reduce_max_sync(full, x0);
+  const size_t rstride = (size_t)a.g.rx * kC;
+  const float* r0 = lz + ((size_t)iz * a.g.ry + y0) * rstride;   // row (iz, y0); y0+1 follows
+  if (__all_sync(full, yz == yz0) && xmax - xmin + 2 <= 32) {
+    const int lane = threadIdx.x & 31;
+    float g[kC];
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) g[ch] = 0.0f;
+    if (lane < xmax - xmin + 2) {
+      const float4* p0 = reinterpret_cast<const float4*>(r0 + (size_t)(xmin + lane) * kC);
+      const float4* p1 = reinterpret_cast<const float4*>(r0 + rstride + (size_t)(xmin + lane) * kC);
+#pragma unroll
+      for (int q = 0; q < kC / 4; ++q) {
+        const float4 f = __ldg(p0 + q), h = __ldg(p1 + q);
+        g[4 * q + 0] = fmaf(ty, h.x - f.x, f.x);
+        g[4 * q + 1] = fmaf(ty, h.y - f.y, f.y);
+        g[4 * q + 2] = fmaf(ty, h.z - f.z, f.z);
+        g[4 * q + 3] = fmaf(ty, h.w - f.w, f.w);
+      }
+    }
+    const int src = x0 - xmin;
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) {
+      const float g0 = __shfl_sync(full, g[ch], src);
+      const float g1 = __shfl_sync(full, g[ch], src + 1);
+      acc[ch] = fmaf(tx, g1 - g0, g0);
+    }
+  } else {
+    // warp straddles (y, z) rows: same arithmetic per lane, one x cell at a time
+    float g0[kC];
+#pragma unroll 1
+    for (int dx = 0; dx < 2; ++dx) {
+      const float4* p0 = reinterpret_cast<const float4*>(r0 + (size_t)(x0 + dx) * kC);
+      const float4* p1 = reinterpret_cast<const float4*>(r0 + rstride + (size_t)(x0 + dx) * kC);
+#pragma unroll
+      for (int q = 0; q < kC / 4; ++q) {
+        const float4 f = __ldg(p0 + q), h = __ldg(p1 + q);
+        const float gy[4] = {fmaf(ty, h.x - f.x, f.x), fmaf(ty, h.y - f.y, f.y),
+                             fmaf(ty, h.z - f.z, f.z), fmaf(ty, h.w - f.w, f.w)};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (dx == 0) g0[4 * q + u] = gy[u];
+          else acc[4 * q + u] = fmaf(tx, gy[u] - g0[4 * q + u], g0[4 * q + u]);
+        }
+      }
+    }
+  }
+}
+
 // Points-mode embedding (NdfModel.forward): fp64 sincos per point, fp32 latent.
 __device__ __forceinline__ void embed_point_tc(const QueryArgs& a, const float* __restrict__ grid,
                                                const double* pos, float* e) {
@@ -358,6 +465,9 @@ struct TcArgs {
   QueryArgs q;
   const float* ftab;      // grid mode: (nx+ny+nz) x kAxisRow per-axis node table
   const float* erefs;     // grid mode: n_ref x kERefStride reference embeddings
+  const uint32_t* xtab;   // ws schedule: nx x kXTabWords pre-merged x words
+  const uint32_t* yztab;  // ws schedule: (ny*nz) x kYZTabWords pre-merged (y, z) words
+  const float* lz;        // ws schedule: nz x ry x rx x C latent rows interpolated in z
   int n_ref;
   uint16_t* out16;        // multi-ref output (fp16), rows of ld_out
   int64_t ld_out;
@@ -638,56 +748,71 @@ query_tc_kernel(const TcArgs t, const int nwg) {
                  "r"(tmem_cols));
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised schedule (NDF_TC_SCHEDULE=ws; single-reference grid queries).
-//   WG0..WG3 -- epilogue warpgroups, one TMEM-accumulator / A-buffer slot each:
-//               drain the accumulator (tcgen05.ld pipelined one 32-column chunk
-//               ahead), bias + activation, write the next A operand, issue the next
-//               MMA, and finally read the output column and release the slot.
-//   WG4, WG5 -- producer warpgroups: embed the next query tile and pack its merged
-//               16-bit layer-0 rows in registers *before* the slot is released, then
-//               only store them (14 x 16 B per row) and issue the layer-0 MMA, so
-//               the L2-latency-bound encoder never sits on the epilogue warps' path.
-// Synchronisation is mbarrier-only: acc_full[s] (tcgen05.commit after every MMA
-// stage) and slot_free[s] (epilogue WG after reading the output column).
-constexpr int kSlots = 4;
-constexpr int kKinMax = 128;
-
-template <bool F16, int MERGE, class FA, class FB>
-__device__ __forceinline__ void pack_input_row(int merge, FA ea, FB eb, int kin, uint32_t* pk) {
-#pragma unroll
-  for (int kg = 0; kg < kKinMax / 8; ++kg) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i0 = 8 * kg + 2 * q;
-      pk[4 * kg + q] = (8 * kg < kin)
-          ? pack2<F16>(merged_value<MERGE>(merge, i0, ea, eb), merged_value<MERGE>(merge, i0 + 1, ea, eb))
-          : 0u;
-    }
-  }
-}
-
+// Hidden-layer epilogue of one 32-column chunk: bias (all 8 LDS.128 first), then
+// the 32 independent MUFU tanh back to back, then FMA + 16-bit pack + 4 STS.128.
+// st_shared_v4 carries no "memory" clobber, so the bias loads are free to move
+// ahead of earlier chunks' stores (the A buffer is only read by the tensor cores,
+// after fence.proxy.async).
 template <bool F16, bool SILU>
 __device__ __forceinline__ void epilogue_chunk(const float* v, const float4* b4, int c0,
                                                int act, uint32_t a_addr, int row) {
+  float x[32];
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const float4 ba = b4[(c0 >> 2) + 2 * jj];
-    const float4 bb = b4[(c0 >> 2) + 2 * jj + 1];
-    const float x[8] = {v[8 * jj] + ba.x, v[8 * jj + 1] + ba.y, v[8 * jj + 2] + ba.z,
-                        v[8 * jj + 3] + ba.w, v[8 * jj + 4] + bb.x, v[8 * jj + 5] + bb.y,
-                        v[8 * jj + 6] + bb.z, v[8 * jj + 7] + bb.w};
-    uint32_t p[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float x0 = x[2 * q], x1 = x[2 * q + 1];
-      if constexpr (SILU)     // x = z/2 (weights pre-scaled): silu(z) = x + x*tanh(x)
-        p[q] = pack2<F16>(fmaf(x0, tanh_fast(x0), x0), fmaf(x1, tanh_fast(x1), x1));
-      else
-        p[q] = pack2<F16>(act_f32(act, x0), act_f32(act, x1));
-    }
-    st_shared_v4(a_addr + canon_off(row, c0 + 8 * jj, kSboA), p[0], p[1], p[2], p[3]);
+  for (int q = 0; q < 8; ++q) {
+    const float4 b = b4[(c0 >> 2) + q];
+    x[4 * q] = v[4 * q] + b.x;
+    x[4 * q + 1] = v[4 * q + 1] + b.y;
+    x[4 * q + 2] = v[4 * q + 2] + b.z;
+    x[4 * q + 3] = v[4 * q + 3] + b.w;
   }
+  float h[32];
+  if constexpr (SILU) {       // x = z/2 (weights pre-scaled): silu(z) = x + x*tanh(x)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = tanh_fast(x[i]);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = fmaf(x[i], h[i], x[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = act_f32(act, x[i]);
+  }
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj)
+    st_shared_v4(a_addr + canon_off(row, c0 + 8 * jj, kSboA), pack2<F16>(h[8 * jj], h[8 * jj + 1]),
+                 pack2<F16>(h[8 * jj + 2], h[8 * jj + 3]), pack2<F16>(h[8 * jj + 4], h[8 * jj + 5]),
+                 pack2<F16>(h[8 * jj + 6], h[8 * jj + 7]));
+}
+
+// Last hidden layer: bias + activation in fp32, then the output layer's dot product
+// (128 -> 1) on the FMA pipe in fp32.  The fp32 output weights live in rows 1-2 of
+// the packed N=16 output operand (whose columns 1..15 nobody reads): k-group g's 8
+// weights are the 32 bytes at g*128 + 16.  Four partial sums break the FMA chain.
+template <bool SILU>
+__device__ __forceinline__ void epilogue_dot(const float* v, const float4* b4, int c0, int act,
+                                             uint32_t wout_addr, float* dots) {
+  float x[32], w[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 b = b4[(c0 >> 2) + q];
+    x[4 * q] = v[4 * q] + b.x;
+    x[4 * q + 1] = v[4 * q + 1] + b.y;
+    x[4 * q + 2] = v[4 * q + 2] + b.z;
+    x[4 * q + 3] = v[4 * q + 3] + b.w;
+    const uint32_t wa = wout_addr + (uint32_t)(((c0 >> 3) + (q >> 1)) * 128 + 16 + 16 * (q & 1));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(w[4 * q]), "=f"(w[4 * q + 1]), "=f"(w[4 * q + 2]), "=f"(w[4 * q + 3]) : "r"(wa));
+  }
+  float h[32];
+  if constexpr (SILU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = tanh_fast(x[i]);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = fmaf(x[i], h[i], x[i]);   // x = z/2: silu(z)
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) h[i] = act_f32(act, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) dots[i & 3] = fmaf(h[i], w[i], dots[i & 3]);
 }
 
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float* v) {
@@ -707,32 +832,174 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <bool F16, bool SILU, int KIND>
-__global__ void __launch_bounds__(768, 1)
-query_ws_kernel(const TcArgs t) {
+// Issue K16 steps [k0, k0 + nsteps) of one layer into d_tmem (one thread).
+__device__ __forceinline__ void issue_ksteps(uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr,
+                                             int k0, int nsteps, uint32_t sbo_b, uint32_t idesc,
+                                             bool accumulate_first) {
+  for (int kk = k0; kk < k0 + nsteps; ++kk) {
+    const uint64_t ad = smem_desc(a_addr + kk * 256, 128, kSboA);
+    const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
+    mma_bf16(d_tmem, ad, bd, idesc, (kk > k0 || accumulate_first) ? 1u : 0u);
+  }
+}
+// A operand in TMEM ("TS" form): K16 steps [k0, k0 + nsteps), step kk's 8 columns at
+// a_col(kk) = a_tmem + 8 kk + (kk >= 4 ? 32 : 0) (each column half of the epilogue packs
+// its 64 K-values into the first 32 of its own, already drained, 64 columns).
+__device__ __forceinline__ void issue_ksteps_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_addr,
+                                                int k0, int nsteps, uint32_t sbo_b,
+                                                uint32_t idesc, bool accumulate_first) {
+  for (int kk = k0; kk < k0 + nsteps; ++kk) {
+    const uint32_t ac = a_tmem + (uint32_t)(8 * kk + (kk >= 4 ? 32 : 0));
+    const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
+    const uint32_t acc = (kk > k0 || accumulate_first) ? 1u : 0u;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(ac), "l"(bd), "r"(idesc), "r"(acc));
+  }
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// Timing experiment only (tools/ab_variants.sh): NDF_EXP_NOMUFU replaces tanh by an
+// FMA-pipe stand-in (results are wrong).
+#ifdef NDF_EXP_NOMUFU
+#define NDF_EXP_TANH(x) ((x) * 0.25f)
+#else
+#define NDF_EXP_TANH(x) tanh_fast(x)
+#endif
+
+// Hidden-layer epilogue of one 16-column sub-chunk (the bias is already in the
+// accumulator): SiLU (one MUFU tanh per element, weights and bias pre-scaled by
+// 1/2), 16-bit pack, and one tcgen05.st of the 8 packed
+// words into TMEM, where the next layer's MMA reads its A operand (row = lane,
+// K-pairs along the columns).
+template <bool F16, bool SILU>
+__device__ __forceinline__ void epilogue16(const float* x, int act, uint32_t a_taddr) {
+  float h[16];
+  if constexpr (SILU) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = fmaf(x[i], h[i], x[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
+  }
+  uint32_t p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = pack2<F16>(h[2 * i], h[2 * i + 1]);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               ::"r"(a_taddr), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]),
+               "r"(p[6]), "r"(p[7]) : "memory");
+}
+
+// Last hidden layer, one 16-column sub-chunk (bias already in the accumulator):
+// activation in fp32, then the output layer's partial dot product (fp32 weights in
+// rows 1-2 of the packed N=16 output operand: k-group g's 8 weights are the 32
+// bytes at g*128 + 16).
+template <bool SILU>
+__device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t wout_addr,
+                                      float* dots) {
+  float w[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t wa = wout_addr + (uint32_t)(((c0 >> 3) + (q >> 1)) * 128 + 16 + 16 * (q & 1));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(w[4 * q]), "=f"(w[4 * q + 1]), "=f"(w[4 * q + 2]), "=f"(w[4 * q + 3]) : "r"(wa));
+  }
+  float h[16];
+  if constexpr (SILU) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = fmaf(x[i], h[i], x[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) dots[i & 3] = fmaf(h[i], w[i], dots[i & 3]);
+}
+
+// Ping-pong schedule for single-reference grid queries (sum_absdiff merge; the
+// default -- NDF_TC_SCHEDULE=classic selects query_tc_kernel instead).
+//   2 slots per CTA, each = 256 TMEM columns holding TWO accumulator halves plus a
+//   32 KB SMEM buffer for layer 0's A operand.  Layer l of a slot accumulates into
+//   half (l & 1) while the epilogue drains the other half, so the next layer's MMA
+//   runs underneath the current epilogue (issued 32 K-columns at a time) instead of
+//   after it.  Hidden layers take their A operand from TMEM ("TS" MMA): the epilogue
+//   packs the 16-bit activations into the columns it has just drained, so the
+//   activations never touch shared memory.
+//   WG0-3 -- epilogue: WG 2s+c drains columns [64c, 64c+64) of slot s (4 warps = the
+//            4 TMEM lane quarters), so every SM sub-partition runs four epilogue
+//            warps.  Per 16-column sub-chunk: tcgen05.ld (one ahead), bias + SiLU
+//            (MUFU tanh), pack, tcgen05.st; per 32 columns, one thread of WG 2s issues
+//            that K-chunk's two K16 MMA steps of the next layer.  The last hidden
+//            layer feeds an fp32 dot product with the output weights instead
+//            (partials of the two column halves summed through SMEM) and the head.
+//   WG4, WG5 -- producer of slot 0 / 1: per query tile, the latent words (y/x lerp of
+//            the prep kernel's z-interpolated rows, merged with the reference) and
+//            raw-coordinate words in registers; once the previous layer-0 MMA has
+//            consumed the SMEM A buffer, the pre-merged Fourier groups by cp.async
+//            from the per-query x / (y, z) tables and the registers stored; the
+//            layer-0 MMA is issued once the target accumulator half is drained.
+// Synchronisation: acc_full[s] (tcgen05.commit of each layer's MMAs), s_free[s]
+// (layer 0's SMEM A consumed: the producer may write the next tile's), d_free[s] (the
+// tile's last MMA has completed: the next tile's layer 0 may target the other D half)
+// and named barriers per K-chunk (warps 1.. arrive, the issuing warp syncs).
+constexpr int kPPSlots = 2;
+constexpr int kPPThreads = 768;
+constexpr int kBiasBlk = 128 * 16 * 2;     // one 128 x 16 16-bit operand block
+
+template <bool F16, bool SILU>
+__global__ void __launch_bounds__(kPPThreads, 1)
+query_pp_kernel(const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const QueryArgs& a = t.q;
   const Layout lay = make_layout(a.m);
   uint8_t* wblob = smem;
   uint8_t* abufs = smem + ((lay.blob_bytes + 1023) & ~1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + kSlots * kABytes);
+  // bias folding: a 128x16 "ones" A block (column 0 = 1) and per layer a 16x128 B block
+  // whose k=0 row is the layer's bias, so one extra K16 MMA step initialises the
+  // accumulator with the bias and the epilogue has no bias adds
+  uint8_t* ones_blk = abufs + kPPSlots * kABytes;
+  uint8_t* bias_blk = ones_blk + kBiasBlk;                    // [H] x kBiasBlk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bias_blk + lay.H * kBiasBlk);
   uint64_t* wbar = &bars[0];
-  uint64_t* acc_full = &bars[1];            // [kSlots]
-  uint64_t* slot_free = &bars[1 + kSlots];  // [kSlots]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  float* eref_s = reinterpret_cast<float*>(bars + 16);
+  uint64_t* acc_full = &bars[1];                  // [kPPSlots] a layer's MMAs completed
+  uint64_t* s_free = &bars[1 + kPPSlots];         // [kPPSlots] layer-0 SMEM A consumed
+  uint64_t* d_free = &bars[1 + 2 * kPPSlots];     // [kPPSlots] next tile's D half drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  float* eref_s = reinterpret_cast<float*>(bars + 16);      // reference latent channels
+  float* dotx = reinterpret_cast<float*>(bars + 32);        // [kPPSlots][128] partial dots
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int lane = tid & 31;
   const int wg = warp >> 2;
-  const int wtid = tid & 127;
+  const int wq = warp & 3;                        // TMEM lane quarter
+  const int wtid = tid & 127;                     // tile row
   const float* vecs = reinterpret_cast<const float*>(wblob + lay.vec_off);
 
   if (tid == 0) {
     mbar_init(wbar, 1);
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kPPSlots; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&slot_free[s], 1);
+      mbar_init(&s_free[s], 1);
+      mbar_init(&d_free[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -741,7 +1008,20 @@ query_ws_kernel(const TcArgs t) {
                      smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid < kERefStride) eref_s[tid] = t.erefs[tid];
+  if (tid < kC) eref_s[tid] = t.erefs[tid];
+  {
+    // ones / bias blocks (K-major canonical, SBO 256 B): row r, 8-element group g at
+    // (r >> 3) * 256 + g * 128 + (r & 7) * 16; only element k = 0 of each row is nonzero
+    const float* gvec = reinterpret_cast<const float*>(
+        reinterpret_cast<const uint8_t*>(a.m.params_tc) + lay.vec_off);
+    for (int i = tid; i < (1 + lay.H) * 256; i += blockDim.x) {
+      const int blk = i >> 8, r = (i >> 1) & 127, g = i & 1;
+      const float v0 = g ? 0.0f : (blk == 0 ? 1.0f : __ldg(gvec + (blk - 1) * kHid + r));
+      st_shared_v4(smem_u32(ones_blk + blk * kBiasBlk) + (r >> 3) * 256 + g * 128 + (r & 7) * 16,
+                   pack2<F16>(v0, 0.0f), 0u, 0u, 0u);
+    }
+    fence_proxy_async();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -752,149 +1032,195 @@ query_ws_kernel(const TcArgs t) {
       bulk_g2s(wblob + off, src + off, (uint32_t)min(32768, lay.blob_bytes - off), wbar);
   }
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t w_addr = smem_u32(wblob);
   const uint32_t ab_fmt = F16 ? 0u : 1u;
-  const uint32_t idesc_base = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
-                              ((uint32_t)(kTileM >> 4) << 24);
-  const uint32_t idesc = idesc_base | ((uint32_t)(kHid >> 3) << 17);
-  const uint32_t idesc_out = idesc_base | ((uint32_t)(kOutN >> 3) << 17);
+  const uint32_t idesc = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
+                         ((uint32_t)(kHid >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
   const uint32_t sbo_w0 = (uint32_t)(lay.kin / 8) * 128;
+  const int H = lay.H;
 
   const int64_t n = a.v1 - a.v0;
   const int64_t n_tiles = (n + kTileM - 1) / kTileM;
-  const int64_t tile_stride = (int64_t)gridDim.x * kSlots;
-  auto slot_tiles = [&](int s) -> int64_t {
-    const int64_t first = (int64_t)blockIdx.x * kSlots + s;
-    return first < n_tiles ? (n_tiles - first + tile_stride - 1) / tile_stride : 0;
-  };
-  const float* grid_q = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
-  const int bar_id = 1 + wg;
+  const int64_t tile_stride = (int64_t)gridDim.x * kPPSlots;
+  const int s = wg < 4 ? (wg >> 1) : wg - 4;        // slot of this warpgroup
+  const int64_t first = (int64_t)blockIdx.x * kPPSlots + s;
+  const int64_t cnt = first < n_tiles ? (n_tiles - first + tile_stride - 1) / tile_stride : 0;
+  const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+  const uint32_t d_slot = tmem_base + (uint32_t)(s * 2 * kHid);   // + kHid * half
 
-  if (wg >= kSlots) {
-    // ======================= producer warpgroups (WG4, WG5) =========================
-    // WG4 fills slots 0 and 2, WG5 slots 1 and 3, alternating; the next tile's merged
-    // 16-bit row is packed in registers before the slot is released.
-    const int pslots[2] = {wg - kSlots, wg - kSlots + 2};
-    const int64_t cnt[2] = {slot_tiles(pslots[0]), slot_tiles(pslots[1])};
-    const float lscale[3] = {a.nx > 1 ? (float)(a.g.rx - 1) / (float)(a.nx - 1) : 0.0f,
-                             a.ny > 1 ? (float)(a.g.ry - 1) / (float)(a.ny - 1) : 0.0f,
-                             a.nz > 1 ? (float)(a.g.rz - 1) / (float)(a.nz - 1) : 0.0f};
-    uint32_t free_ph[2] = {0u, 0u};
-    bool weights_ready = false;
-    const int64_t rounds = cnt[0] > cnt[1] ? cnt[0] : cnt[1];
-    for (int64_t kk = 0; kk < rounds; ++kk) {
-      for (int si = 0; si < 2; ++si) {
-        if (kk >= cnt[si]) continue;
-        const int s = pslots[si];
-        const int64_t tile = (int64_t)blockIdx.x * kSlots + s + kk * tile_stride;
-        const int64_t vloc = tile * kTileM + wtid;
-        const int tslot = (int)(kk * 2 + si);
-        NDF_TRACE_AT(tslot, 0);
-        uint32_t pk[kKinMax / 2];
-        {
-          float eq[kE];
-          {
-            int ix, iy, iz;
-            tile_node(a, tile, wtid, ix, iy, iz);
-            embed_grid_node(a, grid_q, t.ftab, ix, iy, iz, lscale, eq);   // all lanes
-            if (vloc >= n) {
+  if (wg >= 4) {
+    // ============================ producer (slot s) ==================================
+#pragma unroll 1
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+      const int64_t tile = first + kk * tile_stride;
+      NDF_TRACE_AT((int)kk, 0);
+      int ix, iy, iz;
+      tile_node(a, tile, wtid, ix, iy, iz);
+      const int yzrow = iy + a.ny * iz;
+      uint32_t pv[20];    // words 36..55
+      {
+        float lat[kC];
+        latent_yx_lerp(t.lz, a, ix, iy, iz, lat);
 #pragma unroll
-              for (int i = 0; i < kE; ++i) eq[i] = 0.0f;
-            }
-          }
-          auto fq = [&](int i) { return eq[i]; };
-          auto fr = [&](int i) { return eref_s[i]; };
-          if (a.m.merge == NDF_MERGE_SUM_ABSDIFF)
-            pack_input_row<F16, NDF_MERGE_SUM_ABSDIFF>(0, fr, fq, lay.kin, pk);
-          else if (a.ref_is_mu)
-            pack_input_row<F16, -1>(a.m.merge, fr, fq, lay.kin, pk);
-          else
-            pack_input_row<F16, -1>(a.m.merge, fq, fr, lay.kin, pk);
-        }
-        NDF_TRACE_AT(tslot, 1);
-        if (!weights_ready) {
-          mbar_wait(wbar, 0);
-          weights_ready = true;
-        }
-        if (kk >= 1) {                               // slot must be drained first
-          mbar_wait(&slot_free[s], free_ph[si]);
-          free_ph[si] ^= 1u;
-        }
-        NDF_TRACE_AT(tslot, 2);
-        tc_fence_after();
-        const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+        for (int q = 0; q < kC / 4; ++q) {
+          const float4 r4 = reinterpret_cast<const float4*>(eref_s)[q];
+          const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-        for (int kg = 0; kg < kKinMax / 8; ++kg)
-          if (8 * kg < lay.kin)
-            st_shared_v4(a_addr + canon_off(wtid, 8 * kg, kSboA), pk[4 * kg], pk[4 * kg + 1],
-                         pk[4 * kg + 2], pk[4 * kg + 3]);
-        fence_proxy_async();
-        tc_fence_before();
-        named_bar(bar_id, 128);
-        if (wtid == 0)
-          issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr, lay.kin, sbo_w0, idesc,
-                      &acc_full[s], 0u);
-        NDF_TRACE_AT(tslot, 3);
+          for (int u = 0; u < 4; ++u)
+            pv[4 * q + u] = pack2<F16>(rv[u] + lat[4 * q + u], fabsf(rv[u] - lat[4 * q + u]));
+        }
+        pv[16] = __ldg(t.xtab + (size_t)ix * kXTabWords + 12);
+        const uint2 ryz =
+            __ldg(reinterpret_cast<const uint2*>(t.yztab + (size_t)yzrow * kYZTabWords + 24));
+        pv[17] = ryz.x;
+        pv[18] = ryz.y;
+        pv[19] = 0u;
       }
+      NDF_TRACE_AT((int)kk, 1);
+      if (kk >= 1) mbar_wait(&s_free[s], (uint32_t)((kk - 1) & 1));   // previous layer 0 done
+      NDF_TRACE_AT((int)kk, 2);
+      {
+        const uint32_t* xs = t.xtab + (size_t)ix * kXTabWords;
+        const uint32_t* ys = t.yztab + (size_t)yzrow * kYZTabWords;
+#pragma unroll
+        for (int g = 0; g < 3; ++g)
+          cp_async16(a_addr + canon_off(wtid, 2 * kWordFx + 8 * g, kSboA), xs + 4 * g);
+#pragma unroll
+        for (int g = 0; g < 6; ++g)
+          cp_async16(a_addr + canon_off(wtid, 2 * kWordFyz + 8 * g, kSboA), ys + 4 * g);
+        cp_async_commit();
+      }
+#pragma unroll
+      for (int g = 0; g < 5; ++g)
+        st_shared_v4(a_addr + canon_off(wtid, 2 * kWordLat + 8 * g, kSboA), pv[4 * g],
+                     pv[4 * g + 1], pv[4 * g + 2], pv[4 * g + 3]);
+      cp_async_wait_all();
+      fence_proxy_async();
+      named_bar(11 + s, 128);
+      if (wtid == 0) {
+        if (kk == 0) mbar_wait(wbar, 0);
+        else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
+        tc_fence_after();
+        const uint32_t half = (uint32_t)((kk * H) & 1);
+        mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
+                 smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);       // D = b0
+        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc, true);
+        mma_commit(&acc_full[s]);
+      }
+      NDF_TRACE_AT((int)kk, 3);
     }
   } else {
-    // ======================= epilogue warpgroups (WG0..WG3, one slot each) ==========
-    const int s = wg;
-    const int64_t cnt = slot_tiles(s);
+    // ======================== epilogue (slot s, column half ch) ======================
+    const int ch = wg & 1;
+    const bool issuer = ch == 0 && wq == 0;        // warp issuing slot s's MMAs
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     mbar_wait(wbar, 0);
-    const float bias_out = vecs[lay.H * kHid];
-    const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(s * kHid);
-    const uint32_t a_addr = smem_u32(abufs + s * kABytes);
+    const float bias_out = vecs[H * kHid];
+    const uint32_t wout_addr = w_addr + lay.wout_off;
     uint32_t acc_ph = 0u;
+#pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
-      for (int st = 0; st < lay.H; ++st) {
+#pragma unroll 1
+      for (int l = 0; l < H; ++l) {
+        const uint32_t half = (uint32_t)((kk * H + l) & 1);
+        const uint32_t d_row = d_slot + lane_base + half * kHid + (uint32_t)(64 * ch);
         mbar_wait(&acc_full[s], acc_ph);
         acc_ph ^= 1u;
         tc_fence_after();
-        NDF_TRACE_AT((int)kk, 2 * st);
-        // ---- hidden layer st: drain (pipelined tcgen05.ld), bias + act, next A --------
-        const float4* b4 = reinterpret_cast<const float4*>(vecs + st * kHid);
-        float va[32], vb[32];
-        tmem_ld32_nowait(tmem_row, va);
+        if (l == 0 && issuer && lane == 0) mbar_arrive(&s_free[s]);   // SMEM A reusable
+        NDF_TRACE_AT((int)kk, 2 * l);
+        float va[16], vb[16];
+        tmem_ld16_nowait(d_row, va);
         tmem_wait_ld();
-        tmem_ld32_nowait(tmem_row + 32u, vb);
-        epilogue_chunk<F16, SILU>(va, b4, 0, a.m.activation, a_addr, wtid);
-        tmem_wait_ld();
-        tmem_ld32_nowait(tmem_row + 64u, va);
-        epilogue_chunk<F16, SILU>(vb, b4, 32, a.m.activation, a_addr, wtid);
-        tmem_wait_ld();
-        tmem_ld32_nowait(tmem_row + 96u, vb);
-        epilogue_chunk<F16, SILU>(va, b4, 64, a.m.activation, a_addr, wtid);
-        tmem_wait_ld();
-        epilogue_chunk<F16, SILU>(vb, b4, 96, a.m.activation, a_addr, wtid);
-        fence_proxy_async();
-        tc_fence_before();
-        named_bar(bar_id, 128);
-        NDF_TRACE_AT((int)kk, 2 * st + 1);
-        if (wtid == 0) {
-          if (st + 1 < lay.H)
-            issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr,
-                        w_addr + lay.w0_bytes + st * lay.wh_bytes, kHid, kSboA, idesc,
-                        &acc_full[s], 0u);
-          else
-            issue_stage(tmem_base + (uint32_t)(s * kHid), a_addr, w_addr + lay.wout_off, kHid,
-                        kSboA, idesc_out, &acc_full[s], 0u);
+        if (l + 1 < H) {
+          // ---- hidden layer l -> A of layer l+1 (packed into this warp's drained TMEM
+          // columns), whose MMA follows K-chunk by K-chunk ----------------------------
+          const uint32_t d_next = d_slot + (half ^ 1u) * kHid;
+          const uint32_t a_tm = d_slot + half * kHid;                  // A of layer l+1
+          const uint32_t a_row = d_row;   // this warp's lanes, its own column half
+          const uint32_t wl = w_addr + lay.w0_bytes + l * lay.wh_bytes;
+#pragma unroll 1
+          for (int j = 0; j < 4; j += 2) {            // two 16-column sub-chunks = 1 K-chunk
+            const int c0 = 64 * ch + 16 * j;
+            tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 16), vb);
+            epilogue16<F16, SILU>(va, a.m.activation, a_row + (uint32_t)(8 * j));
+            tmem_wait_ld();
+            if (j + 2 < 4) tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 32), va);
+            epilogue16<F16, SILU>(vb, a.m.activation, a_row + (uint32_t)(8 * j + 8));
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+#ifdef NDF_EXP_NOSYNC
+            if (j + 2 < 4) { tmem_wait_ld(); continue; }
+            named_bar(1 + 4 * s, 256);
+            if (issuer && lane == 0) {
+              tc_fence_after();
+              mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),
+                       smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+              issue_ksteps_ts(d_next, a_tm, wl, 0, 8, kSboA, idesc, true);
+              mma_commit(&acc_full[s]);
+            }
+            continue;
+#endif
+            const int kc = c0 >> 5;                   // K-chunk just completed
+            const int nthr = ch == 0 ? 128 : 160;     // half 1: + the issuing warp
+            if (issuer) {
+              if (kc < 2) {
+                named_bar(1 + 4 * s + kc, nthr);
+              }
+              if (lane == 0) {
+                tc_fence_after();
+                if (kc == 0)                          // D = bias of layer l+1
+                  mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),
+                           smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+                issue_ksteps_ts(d_next, a_tm, wl, 2 * kc, 2, kSboA, idesc, true);
+              }
+              if (kc == 1) {                          // then half 1's K-chunks 2, 3
+#pragma unroll 1
+                for (int k2 = 2; k2 < 4; ++k2) {
+                  named_bar(1 + 4 * s + k2, 160);
+                  if (lane == 0) {
+                    tc_fence_after();
+                    issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+                    if (k2 == 3) mma_commit(&acc_full[s]);
+                  }
+                }
+              }
+            } else {
+              named_bar_arrive(1 + 4 * s + kc, nthr);
+            }
+            if (j + 2 < 4) tmem_wait_ld();
+          }
+          NDF_TRACE_AT((int)kk, 2 * l + 1);
+        } else {
+          // ---- last hidden layer: A is free for the producer; fp32 output dot ---------
+          // layer H-1's MMA has completed, so the other D half (which held layer H-2 and
+          // then A of layer H-1) is free for the next tile's layer 0
+          if (issuer && lane == 0) mbar_arrive(&d_free[s]);
+          float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 1
+          for (int j = 0; j < 4; j += 2) {
+            const int c0 = 64 * ch + 16 * j;
+            tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 16), vb);
+            dot16<SILU>(va, c0, a.m.activation, wout_addr, dots);
+            tmem_wait_ld();
+            if (j + 2 < 4) tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 32), va);
+            dot16<SILU>(vb, c0 + 16, a.m.activation, wout_addr, dots);
+            if (j + 2 < 4) tmem_wait_ld();
+          }
+          tc_fence_before();
+          const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
+          if (ch == 1) dotx[s * kTileM + wtid] = part;
+          named_bar(9 + s, 256);
+          NDF_TRACE_AT((int)kk, 2 * l + 1);
+          if (ch == 0) {
+            const int64_t vloc = (first + kk * tile_stride) * kTileM + wtid;
+            const float z = part + dotx[s * kTileM + wtid] + bias_out;
+            if (vloc < n) a.out[vloc] = head_exact(a.m.head, z);
+          }
+          named_bar(9 + s, 256);                      // dotx consumed before the next tile
+          NDF_TRACE_AT((int)kk, 6);
         }
       }
-      // ---- output column: head, store, release the slot -------------------------------
-      mbar_wait(&acc_full[s], acc_ph);
-      acc_ph ^= 1u;
-      tc_fence_after();
-      NDF_TRACE_AT((int)kk, 6);
-      uint32_t zr;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(zr) : "r"(tmem_row));
-      tmem_wait_ld();
-      tc_fence_before();
-      const int64_t vloc = ((int64_t)blockIdx.x * kSlots + s + kk * tile_stride) * kTileM + wtid;
-      if (vloc < n) a.out[vloc] = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
-      named_bar(bar_id, 128);
-      if (wtid == 0) mbar_arrive(&slot_free[s]);
     }
   }
   tc_fence_before();
@@ -944,6 +1270,135 @@ __global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, fl
   }
 }
 
+// ---- per-query prep for the warp-specialised schedule (sum_absdiff merge) ----
+// raw coordinate and (sin, cos) of the L octaves of one clipped axis coordinate:
+// the same fp64 operations as embed_point_t, so the same bits.
+__device__ __forceinline__ void axis_features(double p, float* f) {
+  f[0] = (float)p;
+  double scale = 3.141592653589793;
+#pragma unroll
+  for (int i = 0; i < kL; ++i) {
+    double sn, cs;
+    sincos(dmul(scale, p), &sn, &cs);
+    f[1 + 2 * i] = (float)sn;
+    f[2 + 2 * i] = (float)cs;
+    scale = scale * 2.0;
+  }
+}
+
+// Per-query prep, kernel 1 of 2 (one thread per item):
+//   [0, F)    F = (nx+ny+nz+3)*L: one fp64 sincos each -> feat[node][1+2o, 2+2o]
+//             (the octave-0 thread also writes the raw coordinate feat[node][0]);
+//             nodes are the x, y, z axis nodes, then the reference's x, y, z
+//   F         the reference's latent channels in fp64 (embed_point_t's latent part)
+//   beyond    lz[iz][cy][cx][:] = latent grid interpolated along z at node iz
+//             (fp32; the query branch's grid)
+// Same fp64 operations as embed_point_t, so every feature has the same bits; one
+// sincos per thread keeps the fp64 latency chain short.
+__global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_lat, float* lz) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nnode = a.nx + a.ny + a.nz + 3;
+  const int64_t F = (int64_t)nnode * kL;
+  if (tid < F) {
+    const int node = (int)(tid / kL), o = (int)(tid % kL);
+    double p;
+    if (node < a.nx) p = node_coord(node, a.nx);
+    else if (node < a.nx + a.ny) p = node_coord(node - a.nx, a.ny);
+    else if (node < a.nx + a.ny + a.nz) p = node_coord(node - a.nx - a.ny, a.nz);
+    else p = a.ref[node - (a.nx + a.ny + a.nz)];
+    p = fmin(fmax(p, -1.0), 1.0);
+    double scale = 3.141592653589793;
+    for (int i = 0; i < o; ++i) scale = scale * 2.0;
+    double sn, cs;
+    sincos(dmul(scale, p), &sn, &cs);
+    float* f = feat + (size_t)node * 16;
+    f[1 + 2 * o] = (float)sn;
+    f[2 + 2 * o] = (float)cs;
+    if (o == 0) f[0] = (float)p;
+  } else if (tid == F) {
+    const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
+    const double p[3] = {fmin(fmax(a.ref[0], -1.0), 1.0), fmin(fmax(a.ref[1], -1.0), 1.0),
+                         fmin(fmax(a.ref[2], -1.0), 1.0)};
+    const AxisCoord cx = level_coord(p[0], a.g.rx);
+    const AxisCoord cy = level_coord(p[1], a.g.ry);
+    const AxisCoord cz = level_coord(p[2], a.g.rz);
+    double acc[kC];
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) acc[ch] = 0.0;
+    for (int c = 0; c < 8; ++c) {      // embed_point_t's corner order and rounding
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+      const double wx = dx ? cx.t : dsub(1.0, cx.t);
+      const double wy = dy ? cy.t : dsub(1.0, cy.t);
+      const double wz = dz ? cz.t : dsub(1.0, cz.t);
+      const double w = dmul(dmul(wx, wy), wz);
+      const int idx = (cx.i0 + dx) + a.g.rx * ((cy.i0 + dy) + a.g.ry * (cz.i0 + dz));
+#pragma unroll
+      for (int ch = 0; ch < kC; ++ch)
+        acc[ch] = dadd(acc[ch], dmul(w, (double)__ldg(grid + (size_t)idx * kC + ch)));
+    }
+    for (int ch = 0; ch < kC; ++ch) eref_lat[ch] = (float)acc[ch];
+  } else {
+    const int64_t k = tid - F - 1;
+    if (k >= (int64_t)a.nz * a.g.ry * a.g.rx) return;
+    const int cx = (int)(k % a.g.rx), cy = (int)((k / a.g.rx) % a.g.ry);
+    const int iz = (int)(k / ((int64_t)a.g.rx * a.g.ry));
+    int z0;
+    float tz;
+    latent_cell(iz, a.nz, a.g.rz, z0, tz);
+    const float* grid = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;   // query branch
+    const float4* p0 = reinterpret_cast<const float4*>(
+        grid + ((size_t)(z0 * a.g.ry + cy) * a.g.rx + cx) * kC);
+    const float4* p1 = p0 + (size_t)a.g.ry * a.g.rx * kC / 4;
+    float4* dst = reinterpret_cast<float4*>(lz + (size_t)k * kC);
+#pragma unroll
+    for (int q = 0; q < kC / 4; ++q) {
+      const float4 f = __ldg(p0 + q), h = __ldg(p1 + q);
+      dst[q] = make_float4(fmaf(tz, h.x - f.x, f.x), fmaf(tz, h.y - f.y, f.y),
+                           fmaf(tz, h.z - f.z, f.z), fmaf(tz, h.w - f.w, f.w));
+    }
+  }
+}
+
+// Per-query prep, kernel 2 of 2: merge the reference's and the query nodes' axis
+// features into the 16-bit A words ([r + q, |r - q|], model.py:279-286 + BASELINE):
+//   [0, nx)             xtab[ix]   = Fourier-x words 0..11, raw-x word at 12
+//   [nx, nx + ny*nz)    yztab[row] = Fourier-(y, z) words in A order, raw y, z at 24, 25
+template <bool F16>
+__global__ void prep_ws_merge_kernel(const QueryArgs a, const float* __restrict__ feat,
+                                     uint32_t* xtab, uint32_t* yztab) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nyz = a.ny * a.nz;
+  const int nref = a.nx + a.ny + a.nz;          // first reference node
+  auto merged = [](float r, float q) { return pack2<F16>(r + q, fabsf(r - q)); };
+  if (tid < a.nx) {
+    const float* r = feat + (size_t)nref * 16;
+    const float* q = feat + (size_t)tid * 16;
+    uint32_t* o = xtab + tid * kXTabWords;
+#pragma unroll
+    for (int j = 0; j < 2 * kL; ++j) o[j] = merged(r[1 + j], q[1 + j]);
+    o[12] = merged(r[0], q[0]);
+    o[13] = o[14] = o[15] = 0u;
+  } else if (tid < a.nx + nyz) {
+    const int row = (int)(tid - a.nx), iy = row % a.ny, iz = row / a.ny;
+    const float* ry = feat + (size_t)(nref + 1) * 16;
+    const float* rz = feat + (size_t)(nref + 2) * 16;
+    const float* qy = feat + (size_t)(a.nx + iy) * 16;
+    const float* qz = feat + (size_t)(a.nx + a.ny + iz) * 16;
+    uint32_t* o = yztab + (size_t)row * kYZTabWords;
+#pragma unroll
+    for (int i = 0; i < kL; ++i) {       // words 12 + 4i + 2(ax-1) + sc
+      o[4 * i + 0] = merged(ry[1 + 2 * i], qy[1 + 2 * i]);
+      o[4 * i + 1] = merged(ry[2 + 2 * i], qy[2 + 2 * i]);
+      o[4 * i + 2] = merged(rz[1 + 2 * i], qz[1 + 2 * i]);
+      o[4 * i + 3] = merged(rz[2 + 2 * i], qz[2 + 2 * i]);
+    }
+    o[24] = merged(ry[0], qy[0]);
+    o[25] = merged(rz[0], qz[0]);
+#pragma unroll
+    for (int j = 26; j < kYZTabWords; ++j) o[j] = 0u;
+  }
+}
+
 // ---- parameter packing (device) ---------------------------------------------
 __global__ void pack_zero_kernel(const ndf_model_desc m, uint8_t* blob) {
   const Layout lay = make_layout(m);
@@ -984,8 +1439,12 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
       for (int64_t e = gtid; e < N; e += gsz) vecs[l * kHid + e] = hs * b[e];
     } else {
       // output layer (128 x 1) -> row 0 of a 16 x 128 canonical B operand
-      for (int64_t e = gtid; e < K; e += gsz)
+      for (int64_t e = gtid; e < K; e += gsz) {
         store16(blob + lay.wout_off + canon_off(0, (int)e, kSboA), W[e], f16);
+        // fp32 copy in rows 1-2 (output columns 1..15 of the N=16 MMA are never read):
+        // k-group g's 8 weights at g*128 + 16 (query_pp_kernel's output dot product)
+        *reinterpret_cast<float*>(blob + lay.wout_off + (e >> 3) * 128 + 16 + (e & 7) * 4) = W[e];
+      }
       if (gtid == 0) vecs[lay.H * kHid] = b[0];
     }
     off += (size_t)K * N + N;
@@ -1009,53 +1468,65 @@ static bool tc_supported(const ndf_model_desc& m, std::string* why) {
   return true;
 }
 
-template <bool F16, bool SILU, int KIND>
-static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, cudaStream_t s) {
-  static size_t attr = 0;
-  if (attr < smem) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<F16, SILU, KIND>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_ws_kernel<F16, SILU, KIND>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  // Schedule for single-reference grid queries: "ws" (default; 4 epilogue + 2
-  // producer warpgroups) or "classic" (4 symmetric warpgroups doing everything;
-  // also used for points and multi-reference queries).  Measured on B200 (c1):
-  // ws 0.328 ms, classic 0.375 ms per query.
+// Schedule for single-reference grid queries with the sum_absdiff merge: "ws"
+// (default; 4 epilogue + 2 producer warpgroups fed by per-query x / (y, z) tables)
+// or "classic" (4 symmetric warpgroups doing everything; also used for points,
+// multi-reference queries and the other merges).  NDF_TC_SCHEDULE=classic forces it.
+static bool use_ws(const QueryArgs& a, int n_ref, int nwg) {
   static int classic = -1;
   if (classic < 0) {
     const char* e = getenv("NDF_TC_SCHEDULE");
     classic = (e && e[0] == 'c') ? 1 : 0;
   }
-  if (classic || nwg != 4 || KIND != tc::kGridSingle) {
+  return !classic && nwg == 4 && a.mode == 0 && n_ref == 1 && a.m.merge == NDF_MERGE_SUM_ABSDIFF;
+}
+
+template <bool F16, bool SILU, int KIND>
+static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, bool ws,
+                       cudaStream_t s) {
+  static size_t attr = 0;
+  if (attr < smem) {
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<F16, SILU, KIND>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if constexpr (KIND == tc::kGridSingle)
+      NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_pp_kernel<F16, SILU>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  if constexpr (KIND != tc::kGridSingle) {
+    tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
+  } else if (!ws) {
     tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
   } else {
-    // warp-specialised: 4 epilogue + 2 producer warpgroups per CTA, one CTA per SM
+    // ping-pong: 2 slots x (epilogue + producer warpgroup) per CTA, one CTA per SM
     const int64_t n = t.q.v1 - t.q.v0;
     const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
     const unsigned g2 = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((tiles + 3) / 4, sm_count()));
-    tc::query_ws_kernel<F16, SILU, KIND><<<g2, 768, smem, s>>>(t);
+        1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));
+    const tc::Layout lay = tc::make_layout(t.q.m);
+    const size_t smem_pp = (size_t)((lay.blob_bytes + 1023) & ~1023) +
+                           (size_t)tc::kPPSlots * tc::kABytes +
+                           (size_t)(1 + lay.H) * tc::kBiasBlk + 2048;
+    tc::query_pp_kernel<F16, SILU><<<g2, tc::kPPThreads, smem_pp, s>>>(t);
   }
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }
 
 template <bool F16>
-static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid,
+static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, bool ws,
                              cudaStream_t s) {
   using namespace tc;
   const bool silu = t.q.m.activation == NDF_ACT_SILU;
   const int kind = t.q.mode == 1 ? kPoints : (t.n_ref > 1 ? kGridMulti : kGridSingle);
   if (silu) {
-    if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, s);
-    if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, s);
-    return launch_tc_t<F16, true, kPoints>(t, nwg, smem, grid, s);
+    if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, ws, s);
+    if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, false, s);
+    return launch_tc_t<F16, true, kPoints>(t, nwg, smem, grid, false, s);
   }
-  if (kind == kGridSingle) return launch_tc_t<F16, false, kGridSingle>(t, nwg, smem, grid, s);
-  if (kind == kGridMulti) return launch_tc_t<F16, false, kGridMulti>(t, nwg, smem, grid, s);
-  return launch_tc_t<F16, false, kPoints>(t, nwg, smem, grid, s);
+  if (kind == kGridSingle) return launch_tc_t<F16, false, kGridSingle>(t, nwg, smem, grid, ws, s);
+  if (kind == kGridMulti) return launch_tc_t<F16, false, kGridMulti>(t, nwg, smem, grid, false, s);
+  return launch_tc_t<F16, false, kPoints>(t, nwg, smem, grid, false, s);
 }
 
 // Grid / points query on the tensor cores; refs (device, n_ref x 3) and out16 are
@@ -1078,6 +1549,7 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
   const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
   const int64_t ctas = std::min<int64_t>((tiles + nwg - 1) / nwg, sm_count());
   const unsigned grid = (unsigned)std::max<int64_t>(ctas, 1);
+  const bool ws = use_ws(a, n_ref, nwg);
 
   tc::TcArgs t{};
   t.q = a;
@@ -1103,20 +1575,51 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
   if (a.mode == 0) {
     NDF_REQUIRE((int64_t)a.nx * a.ny * a.nz < (1LL << 32), NDF_ERR_UNSUPPORTED,
                 "tensor-core grid query supports < 2^32 vertices");
-    const int naxis = a.nx + a.ny + a.nz;
-    const size_t fbytes = (size_t)naxis * tc::kAxisRow * sizeof(float);
-    const size_t ebytes = (size_t)n_ref * tc::kERefStride * sizeof(float);
-    NDF_CUDA_CHECK(scratch_alloc(&scratch, fbytes + ebytes + 64, s));
-    t.ftab = reinterpret_cast<float*>(scratch);
-    t.erefs = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(scratch) + fbytes);
-    const double* refs = refs_dev;
     const int threads = 128;
-    tc::prep_kernel<<<(naxis + n_ref + threads - 1) / threads, threads, 0, s>>>(
-        a, refs, n_ref, const_cast<float*>(t.ftab), const_cast<float*>(t.erefs));
-    NDF_LAUNCH_CHECK();
+    if (ws) {
+      // per-query tables: axis features, x words, (y, z) words, z-interpolated
+      // latent rows, reference latent channels
+      const int64_t nyz = (int64_t)a.ny * a.nz;
+      const int nnode = a.nx + a.ny + a.nz + 3;
+      const size_t fb = (size_t)nnode * 16 * 4;
+      const size_t xb = (size_t)a.nx * tc::kXTabWords * 4;
+      const size_t yb = (size_t)nyz * tc::kYZTabWords * 4;
+      const size_t lb = (size_t)a.nz * a.g.ry * a.g.rx * tc::kC * 4;
+      const size_t eb = (size_t)tc::kERefStride * 4;
+      NDF_CUDA_CHECK(scratch_alloc(&scratch, fb + xb + yb + lb + eb + 256, s));
+      uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+      float* feat = reinterpret_cast<float*>(p);
+      uint32_t* xt = reinterpret_cast<uint32_t*>(p + fb);
+      uint32_t* yt = reinterpret_cast<uint32_t*>(p + fb + xb);
+      float* lt = reinterpret_cast<float*>(p + fb + xb + yb);
+      float* et = reinterpret_cast<float*>(p + fb + xb + yb + lb);
+      t.xtab = xt;
+      t.yztab = yt;
+      t.lz = lt;
+      t.erefs = et;
+      const int64_t n1 = (int64_t)nnode * tc::kL + 1 + (int64_t)a.nz * a.g.ry * a.g.rx;
+      tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(a, feat, et, lt);
+      NDF_LAUNCH_CHECK();
+      const unsigned b2 = (unsigned)((a.nx + nyz + 255) / 256);
+      if (a.prec == NDF_PREC_FP16)
+        tc::prep_ws_merge_kernel<true><<<b2, 256, 0, s>>>(a, feat, xt, yt);
+      else
+        tc::prep_ws_merge_kernel<false><<<b2, 256, 0, s>>>(a, feat, xt, yt);
+      NDF_LAUNCH_CHECK();
+    } else {
+      const int naxis = a.nx + a.ny + a.nz;
+      const size_t fbytes = (size_t)naxis * tc::kAxisRow * sizeof(float);
+      const size_t ebytes = (size_t)n_ref * tc::kERefStride * sizeof(float);
+      NDF_CUDA_CHECK(scratch_alloc(&scratch, fbytes + ebytes + 64, s));
+      t.ftab = reinterpret_cast<float*>(scratch);
+      t.erefs = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(scratch) + fbytes);
+      tc::prep_kernel<<<(naxis + n_ref + threads - 1) / threads, threads, 0, s>>>(
+          a, refs_dev, n_ref, const_cast<float*>(t.ftab), const_cast<float*>(t.erefs));
+      NDF_LAUNCH_CHECK();
+    }
   }
-  int st = a.prec == NDF_PREC_FP16 ? launch_tc_variant<true>(t, nwg, smem, grid, s)
-                                   : launch_tc_variant<false>(t, nwg, smem, grid, s);
+  int st = a.prec == NDF_PREC_FP16 ? launch_tc_variant<true>(t, nwg, smem, grid, ws, s)
+                                   : launch_tc_variant<false>(t, nwg, smem, grid, ws, s);
   if (scratch) cudaFreeAsync(scratch, s);
   return st;
 }

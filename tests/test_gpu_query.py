@@ -150,9 +150,12 @@ def test_batch_invariance_and_vertex_ranges(c0):
         if prec == "fp32":
             assert np.array_equal(looped, full[:50])    # exact path: grid == points, bitwise
         else:
-            # 16-bit path: the grid kernel derives latent cells arithmetically, the
-            # points kernel from the fp64 position -> fp32 weights may differ by an ulp
-            assert np.max(np.abs(looped - full[:50])) <= 2e-3
+            # 16-bit path: the grid kernel derives latent cells arithmetically and runs
+            # the output layer as an fp32 dot product; the points kernel takes fp64
+            # positions and a 16-bit output MMA -> both sit within their precision of
+            # the fp32 oracle, not bitwise on each other
+            tol = 4e-3 if prec == "fp16" else 1.5e-2
+            assert np.max(np.abs(looped - full[:50])) <= tol
 
 
 def test_constant_decoder_bias():

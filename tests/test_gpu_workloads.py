@@ -28,9 +28,12 @@ def test_multi_reference_cube_equals_single_queries(precision):
     V = int(np.prod(dims))
     cube = ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims).cpu()
     assert cube.shape == (len(refs), V) and cube.dtype == torch.float16
+    # single-reference queries run the warp-specialised schedule (table-fed encoder,
+    # fp32 output dot product), the cube the classic one: equal within 16-bit precision
+    tol = 4e-3 if precision == "fp16" else 1.5e-2
     for r, ref in enumerate(refs):
         single = ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, dims).cpu()
-        assert torch.equal(cube[r], single.to(torch.float16))
+        assert float((cube[r].float() - single).abs().max()) <= tol
     # vertex sub-range into a strided output
     out = torch.zeros((len(refs), 2000), dtype=torch.float16, device="cuda")
     ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims, 1000, 2500, out=out)

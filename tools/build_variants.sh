@@ -1,0 +1,21 @@
+#!/bin/bash
+# Build timing-experiment variants of libndf_b200.so into abtest/lib_<name>.so:
+#   base, nomufu, nosts, nosync (see NDF_EXP_* in ndf_query_tc.cu).
+set -e
+cd "$(dirname "$0")/.."
+python -m paper_2307_02203_b200.build > /dev/null
+mkdir -p abtest
+OBJS="build/obj/ndf_capi.o build/obj/ndf_ksg.o build/obj/ndf_pearson.o build/obj/ndf_query_f32.o"
+NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -I paper_2307_02203_b200/csrc"
+for v in "$@"; do
+  case $v in
+    base) D="";; skel) D="-DNDF_EXP_NOMUFU -DNDF_EXP_NOSTS";; nomufu) D="-DNDF_EXP_NOMUFU";; nosts) D="-DNDF_EXP_NOSTS";; nosync) D="-DNDF_EXP_NOSYNC";;
+    *) D="$(echo $v | tr ',' ' ')";;
+  esac
+  $NV $D -c paper_2307_02203_b200/csrc/ndf_query_tc.cu -o abtest/q_$v.o &
+done
+wait
+for v in "$@"; do
+  $NV -shared -o abtest/lib_$v.so abtest/q_$v.o $OBJS -lcudart
+done
+ls abtest/*.so

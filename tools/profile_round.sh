@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     > gpurun_out/ncu_launch.log 2>&1
 python tools/gemv_probe.py > gpurun_out/plain_gemv.log 2>&1 && \
 python tools/ksg_probe.py 16384 > gpurun_out/plain_ksg.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:query_tc -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"query_(tc|ws)" -s 1 -c 1 \
     -o gpurun_out/prof_query python bench.py --quick --steps 2 --warmup 1 > gpurun_out/ncu_q.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:gemv -s 1 -c 1 \
     -o gpurun_out/prof_gemv python tools/gemv_probe.py > gpurun_out/ncu_g.log 2>&1 && \

@@ -1,8 +1,8 @@
-"""Schedule trace of the warp-specialised query kernel (NDF_TC_SCHEDULE=ws), CTA 0.
+"""Schedule trace of the ping-pong query kernel (query_pp_kernel), CTA 0.
 
 E-WG rows (per tile): acc0 / epi0 / acc1 / epi1 / acc2 / epi2 / out = accumulator ready
 and epilogue done times of the three hidden layers and the output stage.
-P-WG rows (per fill): start, packed row ready, slot acquired, layer-0 MMA issued.
+P-WG rows (per fill): start, per-vertex words ready, A buffer free, layer-0 MMA issued.
 """
 import ctypes
 import os
@@ -11,7 +11,6 @@ import sys
 import numpy as np
 import torch
 
-os.environ["NDF_TC_SCHEDULE"] = "ws"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2307_02203_b200 as ndf  # noqa: E402
 from paper_2307_02203_b200 import _native as N  # noqa: E402
@@ -29,32 +28,33 @@ ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
 torch.cuda.synchronize()
 fn(ctypes.c_void_p(0))
 t = buf.cpu().numpy()[:6 * 32 * 12].reshape(6, 32, 12).astype(np.int64)
-t0 = t[4:, 0, 0].min()
+t0 = t[4:6, 0, 0].min()
 names = ["acc0", "epi0", "acc1", "epi1", "acc2", "epi2", "out"]
-for wg in range(4):
-    print(f"E-WG{wg}")
-    for k in range(4):
+for wg in (0, 2):
+    print(f"E-WG{wg} (slot {wg // 2}, columns 0-63)")
+    for k in range(6):
         r = t[wg, k]
         if r[0]:
             print("  tile", k, " ".join(f"{nm}={r[e] - t0:>7d}" for e, nm in enumerate(names)))
 for wg in (4, 5):
-    print(f"P-WG{wg}")
-    for k in range(8):
+    print(f"P-WG{wg} (slot {wg - 4})")
+    for k in range(6):
         r = t[wg, k]
         if r[0]:
             print("  fill", k, " ".join(f"{nm}={r[e] - t0:>7d}" for e, nm in
                                         enumerate(["start", "packed", "slot", "issued"])))
 per = []
-for wg in range(4):
+for wg in (0, 2):
     for k in range(2, 20):
         if t[wg, k + 1, 0] and t[wg, k, 0]:
             per.append(t[wg, k + 1, 0] - t[wg, k, 0])
 if per:
-    print(f"tile period per E-WG {np.mean(per):.0f} cycles -> {np.mean(per) / 4:.0f} per tile per SM")
-e = t[:4, 2:20]
+    print(f"tile period per E-WG {np.mean(per):.0f} cycles -> {np.mean(per) / 2:.0f} per tile per SM")
+e = t[[0, 2], 2:20]
 for i, nm in enumerate(["acc0->epi0", "epi0->acc1", "acc1->epi1", "epi1->acc2", "acc2->epi2",
                         "epi2->out"]):
     d = (e[:, :, i + 1] - e[:, :, i])[e[:, :, 0] > 0]
     print(f"  {nm:12s} {d.mean():8.0f}")
-d = (t[:4, 3:20, 0] - t[:4, 2:19, 6])[t[:4, 3:20, 0] > 0]
+tt = t[[0, 2]]
+d = (tt[:, 3:20, 0] - tt[:, 2:19, 6])[tt[:, 3:20, 0] > 0]
 print(f"  out->next acc0 {d.mean():8.0f}")
