@@ -343,11 +343,11 @@ def run_ours(args):
                        "mlp": model.spec.decoder_widths(), "head": model.spec.head_kind,
                        "parallelism": f"vertex-shard x{world} + NCCL all-gather",
                        "l2": "flushed (512 MB write) between timed steps"},
-            "roofline": {"bound": "tensor", "kernel": "ndf::tc::query_tc_kernel",
+            "roofline": {"bound": "tensor", "kernel": "ndf::tc::query_pp_kernel (+ prep_ws_feat_kernel, prep_ws_merge_kernel)",
                          "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_tflops / peak, "peak_kind": f"{peak_kind} bf16 burst",
                          "kernel_ms": kms, "flop_per_launch": FLOP_PER_PAIR * (v1 - v0),
-                         "traffic": traffic.get("query_tc_kernel"),
+                         "traffic": traffic.get("query_pp_kernel"),
                          "sfu_floor_ms": sfu_floor_ms, "sfu_frac": sfu_floor_ms / kms},
             "clocks": clocks,
             "gpu_launches": launches,

@@ -20,7 +20,7 @@ w = W.CONFIGS[1]
 model = W.build_model(w, seed=0, grid_init=1e-4).with_precision("fp16")
 fn = N.load_library().ndf_debug_tc_trace
 fn.argtypes = [ctypes.c_void_p]
-buf = torch.zeros(6 * 32 * 12 + 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(6 * 32 * 12 + 16 + 16 * 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
     ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
 fn(ctypes.c_void_p(buf.data_ptr()))
@@ -58,3 +58,23 @@ for i, nm in enumerate(["acc0->epi0", "epi0->acc1", "acc1->epi1", "epi1->acc2", 
 tt = t[[0, 2]]
 d = (tt[:, 3:20, 0] - tt[:, 2:19, 6])[tt[:, 3:20, 0] > 0]
 print(f"  out->next acc0 {d.mean():8.0f}")
+
+# fine events of E-WG0's layer 1 (relative to acc1): first ld done, sub-chunk 0 done,
+# wait::st of K-chunk 0, K-chunk 0 barrier/issue done, wait::st of K-chunk 1, epi1
+fine = []
+for k in range(2, 20):
+    r = t[0, k]
+    if r[0] and r[7]:
+        fine.append([r[7] - r[2], r[8] - r[2], r[9] - r[2], r[10] - r[2], r[11] - r[2], r[3] - r[2]])
+if fine:
+    f = np.mean(np.array(fine), axis=0)
+    print("layer-1 fine (cycles after acc1): ld0 %.0f  sub0 %.0f  st0 %.0f  kc0 %.0f  st1 %.0f  end %.0f" % tuple(f))
+
+# per-warp stamps of tile 3, layer 1 (E-warps 0..15): start, sub0, st0(K-chunk 0), sub2, st1, end
+w = buf.cpu().numpy()[6 * 32 * 12 + 16:].reshape(16, 8).astype(np.int64)
+if w[0, 0]:
+    base = w[:, 0].min()
+    print("per-warp layer-1 stamps (tile 3), cycles after the first warp starts:")
+    for i in range(16):
+        print(f"  warp {i:2d} (slot {i // 8}, cols {64 * ((i // 4) % 2)}+)", " ".join(
+            f"{x - base:6d}" for x in w[i, [0, 1, 2, 3, 4, 6]]))
