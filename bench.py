@@ -489,6 +489,28 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
                                 "tflops": FLOP_PER_PAIR * 2 * 64 * V / (c3_ms * 1e-3) / 1e12,
                                 "output": "fp16 cube 64 x 1.76M per head"}
     del cube
+    # ---- the reference's own default architecture (HashGrid + encoder
+    # MLPs, exact fp32 path) queried over the config-1 grid ------------------------------
+    mref = ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=0)
+    outr = torch.empty(v1 - v0, dtype=torch.float32, device=dev)
+    f3 = []
+    for i in range(1 + max(1, args.steps // 5)):
+        flush.fill_(float(i))
+        t0.record(stream)
+        ndf.reconstruct_field_device(mref, w.ref_position(), ndf.ROLE_MU, w.dims, v0, v1, out=outr)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            f3.append(t0.elapsed_time(t1))
+    f3_ms = max_over_ranks(statistics.mean(f3), world)
+    if rank == 0:
+        spec = mref.spec
+        line["f3_reference_default"] = {
+            "ms": f3_ms, "vertices": V, "precision": "fp32 (exact, matmul_exact order)",
+            "model": f"reference ModelSpec(): {spec.levels}-level HashGrid 2^{spec.log2_table_size}"
+                     f"x{spec.features_per_level}, encoders {spec.encoder_widths()}, decoder "
+                     f"{spec.decoder_widths()}, {spec.merge} merge, snake_alt, linear head"}
+    del outr, mref
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
         procs = os.cpu_count() or 1

@@ -21,9 +21,10 @@
 extern "C" {
 #endif
 
-#define NDF_ABI_VERSION 1
+#define NDF_ABI_VERSION 2
 #define NDF_MAX_LAYERS 8
 #define NDF_MAX_WIDTH 256
+#define NDF_MAX_LEVELS 16
 
 /* status codes; mapped onto the reference's NdfError tree (errors.py:4-49) */
 typedef enum {
@@ -50,8 +51,16 @@ enum { NDF_PREC_FP32 = 0,   /* SIMT fp32, sequential k-sum (nn.py:18-20 order) *
 
 /*
  * Model descriptor (host struct, device pointers inside).
- * Mirrors ModelSpec/NdfModel (model.py:29-142) for encoder_layers == 0 with
- * one dense latent level per branch (the BASELINE architecture).
+ * Mirrors ModelSpec/NdfModel (model.py:29-142).  Two latent-grid kinds:
+ *   grid_levels == 0: one dense anisotropic level, (rz, ry, rx, C) fp32, grid_res =
+ *                     (rx, ry, rz) -- the BASELINE architecture;
+ *   grid_levels >= 1: the reference HashGrid (encoding.py:120-178): tables
+ *                     (levels, 2^grid_log2_table, C) fp32, isotropic per-level
+ *                     resolution grid_level_res[l], dense index when res^3 <= 2^T,
+ *                     XOR-prime hash otherwise (encoding.py:90-102).
+ * Optional per-branch encoder MLPs (model.py:133-138, nn.py:124-137): enc_layers
+ * affine layers [enc_widths], activation on all but the last; enc_nu == enc_mu for
+ * shared models.  Encoders and hash grids run on the exact fp32 path only.
  */
 typedef struct ndf_model_desc {
   int32_t fourier_octaves;        /* L: 6L Fourier features (encoding.py:22-51) */
@@ -68,6 +77,14 @@ typedef struct ndf_model_desc {
   const float* params_f32;        /* device: W0 (in x h1, row-major), b0, W1, b1, ...
                                      -- the NDFM/parameters() order (model.py:148-157) */
   const void* params_tc;          /* device: ndf_tc_pack() output, or NULL */
+  /* --- ABI 2: reference HashGrid + encoder MLPs --- */
+  int32_t grid_levels;            /* 0 = dense anisotropic level; >= 1 = HashGrid levels */
+  int32_t grid_log2_table;        /* T: rows per level = 2^T (HashGrid only) */
+  int32_t grid_level_res[NDF_MAX_LEVELS]; /* round(base * growth^l) (encoding.py:82-83) */
+  int32_t enc_layers;             /* encoder affine layers (0 = identity passthrough) */
+  int32_t enc_widths[NDF_MAX_LAYERS + 1]; /* [embed_dim, channels, ...] */
+  const float* enc_mu;            /* device: encoder W0, b0, ... (parameters() order) */
+  const float* enc_nu;            /* device; == enc_mu for shared models */
 } ndf_model_desc;
 
 int32_t ndf_abi_version(void);

@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(HERE, "libndf_b200.so")
 
 NDF_MAX_LAYERS = 8
 NDF_MAX_WIDTH = 256
+NDF_MAX_LEVELS = 16
+NDF_ABI_VERSION = 2
 
 MERGE = {"multiply": 0, "concat": 1, "add": 2, "absdiff": 3, "sum_absdiff": 4}
 ACT = {"relu": 0, "snake": 1, "snake_alt": 2, "silu": 3}
@@ -48,6 +50,14 @@ class ModelDesc(ctypes.Structure):
         ("grid_nu", _c_p),
         ("params_f32", _c_p),
         ("params_tc", _c_p),
+        # ABI 2: reference HashGrid + encoder MLPs
+        ("grid_levels", _i32),
+        ("grid_log2_table", _i32),
+        ("grid_level_res", _i32 * NDF_MAX_LEVELS),
+        ("enc_layers", _i32),
+        ("enc_widths", _i32 * (NDF_MAX_LAYERS + 1)),
+        ("enc_mu", _c_p),
+        ("enc_nu", _c_p),
     ]
 
 
@@ -99,7 +109,7 @@ def load_library(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ndf_abi_version() != 1:
+        if lib.ndf_abi_version() != NDF_ABI_VERSION:
             raise DeviceError("libndf_b200 ABI version mismatch")
         _lib = lib
         return lib

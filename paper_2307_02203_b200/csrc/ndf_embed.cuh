@@ -15,7 +15,7 @@
 
 namespace ndf {
 
-constexpr int kMaxEmbed = 3 + 6 * 12 + 64;   // L <= 12, C <= 64
+constexpr int kMaxEmbed = 3 + 6 * 12 + 64;   // L <= 12, latent (levels * C) <= 64
 
 struct AxisCoord {
   int i0;
@@ -39,9 +39,12 @@ __device__ __forceinline__ AxisCoord level_coord(double p, int res) {
 
 struct EmbedGeom {
   int L;         // Fourier octaves
-  int C;         // latent channels
+  int C;         // latent channels (per level for HashGrids)
   int rx, ry, rz;
-  int E;         // 3 + 6L + C
+  int levels;    // 0: dense anisotropic level (rx, ry, rz); >= 1: HashGrid levels
+  int log2T;     // HashGrid rows per level = 2^log2T
+  int lres[NDF_MAX_LEVELS];
+  int E;         // 3 + 6L + max(levels, 1) * C
 };
 
 __host__ __device__ inline EmbedGeom make_geom(const ndf_model_desc& m) {
@@ -51,8 +54,21 @@ __host__ __device__ inline EmbedGeom make_geom(const ndf_model_desc& m) {
   g.rx = m.grid_res[0];
   g.ry = m.grid_res[1];
   g.rz = m.grid_res[2];
-  g.E = 3 + 6 * g.L + g.C;
+  g.levels = m.grid_levels;
+  g.log2T = m.grid_log2_table;
+  for (int l = 0; l < NDF_MAX_LEVELS; ++l) g.lres[l] = m.grid_level_res[l];
+  g.E = 3 + 6 * g.L + (g.levels > 0 ? g.levels : 1) * g.C;
   return g;
+}
+
+// Table row of lattice corner (ix, iy, iz) on a HashGrid level of resolution res
+// (encoding.py:90-102): dense when res^3 <= 2^T, else (ix*1 ^ iy*2654435761 ^
+// iz*805459861) mod 2^T -- the low bits of the reference's uint64 products.
+__device__ __forceinline__ int64_t hash_row(int res, int log2T, int ix, int iy, int iz) {
+  const int64_t T = (int64_t)1 << log2T;
+  if ((int64_t)res * res * res <= T) return (int64_t)ix + (int64_t)res * (iy + (int64_t)res * iz);
+  const uint64_t h = (uint64_t)ix * 1ull ^ (uint64_t)iy * 2654435761ull ^ (uint64_t)iz * 805459861ull;
+  return (int64_t)(h & (uint64_t)(T - 1));
 }
 
 // Write the fp32 embedding of position (px, py, pz) into out[0..E) via a
@@ -75,6 +91,39 @@ __device__ __forceinline__ void embed_point(const EmbedGeom& g, const float* __r
       store(3 + 6 * i + 2 * ax + 1, (float)c);
     }
     scale = scale * 2.0;
+  }
+  if (g.levels > 0) {
+    // HashGrid (encoding.py:149-178): per level, trilinear over the 8 corners in
+    // _CORNER_OFFSETS order, weights ((1*wx)*wy)*wz and the corner sum in fp64,
+    // output concatenated coarse to fine.
+    const int64_t T = (int64_t)1 << g.log2T;
+    for (int lv = 0; lv < g.levels; ++lv) {
+      const int res = g.lres[lv];
+      const AxisCoord cx = level_coord(p[0], res);
+      const AxisCoord cy = level_coord(p[1], res);
+      const AxisCoord cz = level_coord(p[2], res);
+      double w[8];
+      int64_t row[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+        const double wx = dx ? cx.t : dsub(1.0, cx.t);
+        const double wy = dy ? cy.t : dsub(1.0, cy.t);
+        const double wz = dz ? cz.t : dsub(1.0, cz.t);
+        w[c] = dmul(dmul(wx, wy), wz);
+        row[c] = hash_row(res, g.log2T, cx.i0 + dx, cy.i0 + dy, cz.i0 + dz);
+      }
+      const float* tab = grid + (size_t)lv * (size_t)T * g.C;
+      const int base = 3 + 6 * g.L + lv * g.C;
+      for (int ch = 0; ch < g.C; ++ch) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          acc = dadd(acc, dmul(w[c], (double)__ldg(tab + (size_t)row[c] * g.C + ch)));
+        store(base + ch, (float)acc);
+      }
+    }
+    return;
   }
   const AxisCoord cx = level_coord(p[0], g.rx);
   const AxisCoord cy = level_coord(p[1], g.ry);

@@ -1,12 +1,14 @@
-// Exact fp32 NDF query (SIMT): embed -> merge -> decoder -> head.
+// Exact fp32 NDF query (SIMT): embed -> [encoder MLP] -> merge -> decoder -> head.
 //
-// The decoder matmul restates matmul_exact (nn.py:18-20): z_j = sum_k h_k w_kj
+// Every matmul restates matmul_exact (nn.py:18-20): z_j = sum_k h_k w_kj
 // accumulated sequentially in ascending k with separately rounded multiply and
 // add (no FMA contraction), bias added afterwards (nn.py:135) -- bit-identical
 // to the reference's einsum.  Hidden activations / heads use libdevice fp32
 // transcendentals (<= 2 ulp from NumPy's), so outputs agree to ~1e-7.
 //
-// Used for BASELINE config 0 (fp32) and as the exact mode of every query.
+// Covers both latent-grid kinds (dense anisotropic level, reference HashGrid)
+// and the reference's per-branch encoder MLPs (model.py:179-189), i.e. the
+// reference default architecture as well as BASELINE config 0.
 // Tile: 128 threads, 32 query vertices; activations staged k-major in SMEM so
 // each k step reads the tile's 32 activations as 8 broadcast LDS.128.
 #include <algorithm>
@@ -18,69 +20,195 @@ namespace ndf {
 constexpr int kTV = 32;               // vertices per tile
 constexpr int kTVP = kTV + 4;         // padded k-row stride (floats)
 constexpr int kThreadsF32 = 128;
+constexpr int kBufFloats = NDF_MAX_WIDTH * kTVP;
 
+__device__ __forceinline__ int enc_out_dim(const ndf_model_desc& m, int E) {
+  return m.enc_layers > 0 ? m.enc_widths[m.enc_layers] : E;
+}
+
+// One dense layer over the tile: Hout[j][v] = act(sum_k Hin[k][v] W[k][j] + b[j]) for
+// j < N (sequential ascending k, unfused fp32 -- matmul_exact); `act` false = linear.
+__device__ __forceinline__ void tile_layer(const float* Hin, float* Hout, const float* W,
+                                           const float* b, int K, int N, bool act, int kind) {
+  for (int j = threadIdx.x; j < N; j += kThreadsF32) {
+    float acc[kTV];
+#pragma unroll
+    for (int v = 0; v < kTV; ++v) acc[v] = 0.0f;
+    for (int k = 0; k < K; ++k) {
+      const float w = __ldg(W + (size_t)k * N + j);
+      const float4* hr = reinterpret_cast<const float4*>(Hin + k * kTVP);
+#pragma unroll
+      for (int q = 0; q < kTV / 4; ++q) {
+        const float4 h = hr[q];
+        acc[4 * q + 0] = fadd(acc[4 * q + 0], fmul(h.x, w));
+        acc[4 * q + 1] = fadd(acc[4 * q + 1], fmul(h.y, w));
+        acc[4 * q + 2] = fadd(acc[4 * q + 2], fmul(h.z, w));
+        acc[4 * q + 3] = fadd(acc[4 * q + 3], fmul(h.w, w));
+      }
+    }
+    const float bj = __ldg(b + j);
+    float4* ho = reinterpret_cast<float4*>(Hout + j * kTVP);
+#pragma unroll
+    for (int q = 0; q < kTV / 4; ++q) {
+      float o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float z = fadd(acc[4 * q + u], bj);
+        o[u] = act ? act_exact(kind, z) : z;
+      }
+      ho[q] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  __syncthreads();
+}
+
+// Encoder MLP over the tile (Mlp.forward, nn.py:124-137): activation on all layers
+// but the last.  Input in *bufs[0]; returns the buffer holding the output.
+__device__ __forceinline__ float* tile_encoder(const ndf_model_desc& m, const float* P,
+                                               float* in, float* other) {
+  size_t off = 0;
+  float* hin = in;
+  float* hout = other;
+  for (int l = 0; l < m.enc_layers; ++l) {
+    const int K = m.enc_widths[l], N = m.enc_widths[l + 1];
+    const float* W = P + off;
+    const float* b = W + (size_t)K * N;
+    off += (size_t)K * N + N;
+    tile_layer(hin, hout, W, b, K, N, l + 1 < m.enc_layers, m.activation);
+    float* t = hin; hin = hout; hout = t;
+  }
+  return hin;
+}
+
+// Encoder MLP of ONE vector (the reference point): threads j < N, ping-pong in SMEM.
+__device__ __forceinline__ float* vec_encoder(const ndf_model_desc& m, const float* P, float* x,
+                                              float* y) {
+  size_t off = 0;
+  for (int l = 0; l < m.enc_layers; ++l) {
+    const int K = m.enc_widths[l], N = m.enc_widths[l + 1];
+    const float* W = P + off;
+    const float* b = W + (size_t)K * N;
+    off += (size_t)K * N + N;
+    for (int j = threadIdx.x; j < N; j += kThreadsF32) {
+      float acc = 0.0f;
+      for (int k = 0; k < K; ++k) acc = fadd(acc, fmul(x[k], __ldg(W + (size_t)k * N + j)));
+      const float z = fadd(acc, __ldg(b + j));
+      y[j] = l + 1 < m.enc_layers ? act_exact(m.activation, z) : z;
+    }
+    __syncthreads();
+    float* t = x; x = y; y = t;
+  }
+  return x;
+}
+
+// merge (model.py:279-286 + sum_absdiff) of branch values a (mu) and b (nu) into row
+// i (and C + i for the two-block merges) of the decoder input
+__device__ __forceinline__ void merge_store(int mode, int C, int i, int v, float av, float bv,
+                                            float* D) {
+  switch (mode) {
+    case NDF_MERGE_MULTIPLY: D[i * kTVP + v] = fmul(av, bv); break;
+    case NDF_MERGE_CONCAT: D[i * kTVP + v] = av; D[(C + i) * kTVP + v] = bv; break;
+    case NDF_MERGE_ADD: D[i * kTVP + v] = fadd(av, bv); break;
+    case NDF_MERGE_ABSDIFF: D[i * kTVP + v] = fabsf(__fsub_rn(av, bv)); break;
+    default:
+      D[i * kTVP + v] = fadd(av, bv);
+      D[(C + i) * kTVP + v] = fabsf(__fsub_rn(av, bv));
+      break;
+  }
+}
+
+// SMEM: B0, B1 [NDF_MAX_WIDTH][kTVP] (+ B2 for points mode: the mu branch), then two
+// NDF_MAX_WIDTH vectors for the reference's embedding / encoding.
 __global__ void __launch_bounds__(kThreadsF32)
 query_f32_kernel(const QueryArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int Wmax = NDF_MAX_WIDTH;
-  float* H0 = smem;                          // [Wmax][kTVP] k-major
-  float* H1 = H0 + Wmax * kTVP;
-  float* e_ref = H1 + Wmax * kTVP;           // [kMaxEmbed]
-  float* e_q = e_ref + kMaxEmbed;            // [kTV][kMaxEmbed]
+  float* B0 = smem;
+  float* B1 = B0 + kBufFloats;
+  float* B2 = B1 + kBufFloats;                 // points mode only
+  float* rv0 = a.mode == 1 ? B2 + kBufFloats : B2;
+  float* rv1 = rv0 + NDF_MAX_WIDTH;
 
   const int tid = threadIdx.x;
   const EmbedGeom& g = a.g;
   const int E = g.E;
+  const int Cenc = enc_out_dim(a.m, E);
   const int64_t n_vert = a.v1 - a.v0;
   const float* P = a.m.params_f32;
+  const float* enc_ref = a.ref_is_mu ? a.m.enc_mu : a.m.enc_nu;
+  const float* enc_q = a.ref_is_mu ? a.m.enc_nu : a.m.enc_mu;
 
-  if (a.mode == 0 && tid == 0) {
-    const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
-    embed_point(g, grid, a.ref[0], a.ref[1], a.ref[2], [&](int i, float v) { e_ref[i] = v; });
+  // ---- reference branch (grid mode): embedded and encoded once per CTA ----------
+  float* eref = rv0;
+  if (a.mode == 0) {
+    if (tid == 0) {
+      const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
+      embed_point(g, grid, a.ref[0], a.ref[1], a.ref[2], [&](int i, float v) { rv0[i] = v; });
+    }
+    __syncthreads();
+    if (a.m.enc_layers > 0) eref = vec_encoder(a.m, enc_ref, rv0, rv1);
   }
-  __syncthreads();
 
   for (int64_t tile = blockIdx.x; tile * kTV < n_vert; tile += gridDim.x) {
     const int64_t base = a.v0 + tile * kTV;
     const int nv = (int)min((int64_t)kTV, a.v1 - base);
-    // ---- embed + merge: one thread per vertex ------------------------------
+    // ---- embed: one thread per vertex, written k-major into column v ------------
     if (tid < kTV) {
       const int v = tid;
-      float* eq = e_q + v * kMaxEmbed;
       if (v < nv) {
         const int64_t gv = base + v;
         if (a.mode == 0) {
           double p[3];
           vertex_position(a, gv, p);
           const float* grid = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
-          embed_point(g, grid, p[0], p[1], p[2], [&](int i, float x) { eq[i] = x; });
-          auto ld_r = [&](int i) { return e_ref[i]; };
-          auto ld_q = [&](int i) { return eq[i]; };
-          auto st = [&](int i, float x) { H0[i * kTVP + v] = x; };
-          if (a.ref_is_mu) merge_into(a.m.merge, E, ld_r, ld_q, st);
-          else merge_into(a.m.merge, E, ld_q, ld_r, st);
+          embed_point(g, grid, p[0], p[1], p[2], [&](int i, float x) { B0[i * kTVP + v] = x; });
         } else {
           const int64_t im = a.n_mu == 1 ? 0 : gv;
-          float* em = eq;
-          // mu embedding into e_q row, nu embedding into the H1 scratch column
           embed_point(g, a.m.grid_mu, a.p_mu[3 * im], a.p_mu[3 * im + 1], a.p_mu[3 * im + 2],
-                      [&](int i, float x) { em[i] = x; });
+                      [&](int i, float x) { B2[i * kTVP + v] = x; });
           embed_point(g, a.m.grid_nu, a.p_nu[3 * gv], a.p_nu[3 * gv + 1], a.p_nu[3 * gv + 2],
-                      [&](int i, float x) { H1[i * kTVP + v] = x; });
-          auto ld_m = [&](int i) { return em[i]; };
-          auto ld_n = [&](int i) { return H1[i * kTVP + v]; };
-          auto st = [&](int i, float x) { H0[i * kTVP + v] = x; };
-          merge_into(a.m.merge, E, ld_m, ld_n, st);
+                      [&](int i, float x) { B0[i * kTVP + v] = x; });
         }
       } else {
-        const int din = a.m.widths[0];
-        for (int i = 0; i < din; ++i) H0[i * kTVP + v] = 0.0f;
+        for (int i = 0; i < E; ++i) {
+          B0[i * kTVP + v] = 0.0f;
+          if (a.mode == 1) B2[i * kTVP + v] = 0.0f;
+        }
       }
     }
     __syncthreads();
-    // ---- decoder ------------------------------------------------------------
-    float* Hin = H0;
-    float* Hout = H1;
+    // ---- encoders (query branch; points mode: both branches) ---------------------
+    float* q = B0;              // query / nu branch values, Cenc rows
+    float* mu = B2;             // points mode: mu branch values
+    float* free_buf = B1;
+    if (a.m.enc_layers > 0) {
+      q = tile_encoder(a.m, a.mode == 0 ? enc_q : a.m.enc_nu, B0, B1);
+      free_buf = q == B0 ? B1 : B0;
+      if (a.mode == 1) {
+        mu = tile_encoder(a.m, a.m.enc_mu, B2, free_buf);
+        if (mu != B2) {           // result landed in free_buf: B2 is free now
+          float* t = free_buf; free_buf = B2; (void)t;
+        }
+      }
+    }
+    // ---- merge into the decoder input -----------------------------------------------
+    float* D = free_buf;
+    for (int e = tid; e < Cenc * kTV; e += kThreadsF32) {
+      const int i = e / kTV, v = e % kTV;
+      float av, bv;
+      if (a.mode == 0) {
+        const float r = eref[i], x = q[i * kTVP + v];
+        av = a.ref_is_mu ? r : x;
+        bv = a.ref_is_mu ? x : r;
+      } else {
+        av = mu[i * kTVP + v];
+        bv = q[i * kTVP + v];
+      }
+      merge_store(a.m.merge, Cenc, i, v, av, bv, D);
+    }
+    __syncthreads();
+    // ---- decoder ------------------------------------------------------------------
+    float* Hin = D;
+    float* Hout = D == B0 ? B1 : B0;
     size_t off = 0;
     const int L = a.m.n_layers;
     for (int l = 0; l < L; ++l) {
@@ -97,58 +225,52 @@ query_f32_kernel(const QueryArgs a) {
           const float z = fadd(acc, __ldg(b));
           a.out[base - a.v0 + tid] = head_exact(a.m.head, z);
         }
+        __syncthreads();
       } else {
-        for (int j = tid; j < N; j += kThreadsF32) {
-          float acc[kTV];
-#pragma unroll
-          for (int v = 0; v < kTV; ++v) acc[v] = 0.0f;
-          for (int k = 0; k < K; ++k) {
-            const float w = __ldg(W + (size_t)k * N + j);
-            const float4* hr = reinterpret_cast<const float4*>(Hin + k * kTVP);
-#pragma unroll
-            for (int q = 0; q < kTV / 4; ++q) {
-              const float4 h = hr[q];
-              acc[4 * q + 0] = fadd(acc[4 * q + 0], fmul(h.x, w));
-              acc[4 * q + 1] = fadd(acc[4 * q + 1], fmul(h.y, w));
-              acc[4 * q + 2] = fadd(acc[4 * q + 2], fmul(h.z, w));
-              acc[4 * q + 3] = fadd(acc[4 * q + 3], fmul(h.w, w));
-            }
-          }
-          const float bj = __ldg(b + j);
-          float4* ho = reinterpret_cast<float4*>(Hout + j * kTVP);
-#pragma unroll
-          for (int q = 0; q < kTV / 4; ++q) {
-            float4 o;
-            o.x = act_exact(a.m.activation, fadd(acc[4 * q + 0], bj));
-            o.y = act_exact(a.m.activation, fadd(acc[4 * q + 1], bj));
-            o.z = act_exact(a.m.activation, fadd(acc[4 * q + 2], bj));
-            o.w = act_exact(a.m.activation, fadd(acc[4 * q + 3], bj));
-            ho[q] = o;
-          }
-        }
+        tile_layer(Hin, Hout, W, b, K, N, true, a.m.activation);
+        float* t = Hin; Hin = Hout; Hout = t;
       }
-      __syncthreads();
-      float* t = Hin; Hin = Hout; Hout = t;
     }
   }
 }
 
-size_t query_f32_smem_bytes() {
-  return sizeof(float) * (2 * NDF_MAX_WIDTH * kTVP + kMaxEmbed + kTV * kMaxEmbed);
+size_t query_f32_smem_bytes(int mode) {
+  return sizeof(float) * ((mode == 1 ? 3 : 2) * (size_t)kBufFloats + 2 * NDF_MAX_WIDTH);
 }
 
 int validate_model(const ndf_model_desc* m) {
   NDF_REQUIRE(m != nullptr, NDF_ERR_PARAMETER, "null model descriptor");
   NDF_REQUIRE(m->fourier_octaves >= 0 && m->fourier_octaves <= 12, NDF_ERR_UNSUPPORTED,
               "fourier_octaves must be in [0, 12]");
-  NDF_REQUIRE(m->grid_channels >= 1 && m->grid_channels <= 64, NDF_ERR_UNSUPPORTED,
-              "grid_channels must be in [1, 64]");
-  for (int i = 0; i < 3; ++i)
-    NDF_REQUIRE(m->grid_res[i] >= 2, NDF_ERR_CONFIG, "latent resolution must be >= 2 per axis");
+  NDF_REQUIRE(m->grid_levels >= 0 && m->grid_levels <= NDF_MAX_LEVELS, NDF_ERR_UNSUPPORTED,
+              "grid_levels must be in [0, 16]");
+  const int nlev = m->grid_levels > 0 ? m->grid_levels : 1;
+  NDF_REQUIRE(m->grid_channels >= 1 && nlev * m->grid_channels <= 64, NDF_ERR_UNSUPPORTED,
+              "latent features (levels x channels) must be in [1, 64]");
+  if (m->grid_levels == 0) {
+    for (int i = 0; i < 3; ++i)
+      NDF_REQUIRE(m->grid_res[i] >= 2, NDF_ERR_CONFIG, "latent resolution must be >= 2 per axis");
+  } else {
+    NDF_REQUIRE(m->grid_log2_table >= 1 && m->grid_log2_table < 31, NDF_ERR_CONFIG,
+                "log2 table size must be in [1, 31)");
+    for (int l = 0; l < m->grid_levels; ++l)
+      NDF_REQUIRE(m->grid_level_res[l] >= 2, NDF_ERR_CONFIG, "level resolution must be >= 2");
+  }
+  const int E = 3 + 6 * m->fourier_octaves + nlev * m->grid_channels;
+  NDF_REQUIRE(m->enc_layers >= 0 && m->enc_layers <= NDF_MAX_LAYERS, NDF_ERR_UNSUPPORTED,
+              "encoder layer count out of range");
+  int Cenc = E;
+  if (m->enc_layers > 0) {
+    NDF_REQUIRE(m->enc_widths[0] == E, NDF_ERR_SHAPE, "encoder input width != embedding width");
+    for (int i = 0; i <= m->enc_layers; ++i)
+      NDF_REQUIRE(m->enc_widths[i] >= 1 && m->enc_widths[i] <= NDF_MAX_WIDTH, NDF_ERR_UNSUPPORTED,
+                  "encoder width out of range (1..256)");
+    NDF_REQUIRE(m->enc_mu && m->enc_nu, NDF_ERR_PARAMETER, "null encoder parameters");
+    Cenc = m->enc_widths[m->enc_layers];
+  }
   NDF_REQUIRE(m->n_layers >= 1 && m->n_layers <= NDF_MAX_LAYERS, NDF_ERR_UNSUPPORTED,
               "decoder layer count out of range");
-  const int E = 3 + 6 * m->fourier_octaves + m->grid_channels;
-  const int din = (m->merge == NDF_MERGE_SUM_ABSDIFF || m->merge == NDF_MERGE_CONCAT) ? 2 * E : E;
+  const int din = (m->merge == NDF_MERGE_SUM_ABSDIFF || m->merge == NDF_MERGE_CONCAT) ? 2 * Cenc : Cenc;
   NDF_REQUIRE(m->widths[0] == din, NDF_ERR_SHAPE, "decoder input width does not match merge");
   NDF_REQUIRE(m->widths[m->n_layers] == 1, NDF_ERR_CONFIG, "decoder must emit one scalar");
   for (int i = 0; i <= m->n_layers; ++i)
@@ -164,10 +286,10 @@ int validate_model(const ndf_model_desc* m) {
 
 int launch_query_f32(const QueryArgs& a, cudaStream_t s) {
   static bool attr_set = false;
-  const size_t smem = query_f32_smem_bytes();
+  const size_t smem = query_f32_smem_bytes(a.mode);
   if (!attr_set) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(query_f32_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NDF_CUDA_CHECK(cudaFuncSetAttribute(query_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)query_f32_smem_bytes(1)));
     attr_set = true;
   }
   const int64_t n = a.v1 - a.v0;

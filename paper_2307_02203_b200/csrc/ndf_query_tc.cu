@@ -1455,6 +1455,8 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
 
 static bool tc_supported(const ndf_model_desc& m, std::string* why) {
   auto fail = [&](const char* s) { if (why) *why = s; return false; };
+  if (m.grid_levels != 0 || m.enc_layers != 0)
+    return fail("tcgen05 path needs one dense latent level and no encoder MLPs");
   if (m.fourier_octaves != tc::kL || m.grid_channels != tc::kC)
     return fail("tcgen05 path needs fourier_octaves=6 and 16 latent channels");
   if (m.n_layers < 2) return fail("tcgen05 path needs >= 1 hidden layer");

@@ -6,11 +6,16 @@ anisotropic latent grid (``grid_resolution``), the ``sum_absdiff`` merge,
 SiLU hidden activations, a tanh/softplus ``head`` and the query
 ``precision`` ("fp32" = exact SIMT kernel, "bf16" = tcgen05 kernel).
 
-The GPU path covers the encoder-less family (``encoder_layers == 0``) with one
-dense latent level per branch -- BASELINE's architecture and the reference's
-``encoder_layers=0`` single-dense-level ablation.  Multi-level hashed grids
-and encoder MLPs (the reference default) are SURVEY row F3 ("next") and are
-rejected with ConfigError rather than silently evaluated on the CPU.
+Two model families share the GPU path:
+
+* dense: one dense latent level per branch, no encoder MLP -- BASELINE's
+  architecture (anisotropic ``grid_resolution``) and the reference's
+  ``encoder_layers=0`` single-dense-level ablation; every precision;
+* reference: the reference's own architecture -- multi-level
+  HashGrid tables ``(levels, 2^T, F)`` (encoding.py:120-178), per-branch
+  encoder MLPs (model.py:131-142) and any merge -- on the exact fp32 kernel.
+  ``ModelSpec.reference_default()`` is the reference ModelSpec() default
+  (SnakeAlt, linear head), and reference NDFM files load unchanged.
 """
 
 from __future__ import annotations
@@ -96,6 +101,22 @@ class ModelSpec:
         return "tanh" if self.measure_kind == "pearson" else "softplus"
 
     @property
+    def hash_grid(self) -> bool:
+        """True for the reference family: HashGrid tables and/or encoder MLPs."""
+        if self.grid_resolution is not None:
+            return False
+        r0 = int(round(self.base_resolution))
+        return (self.levels > 1 or self.encoder_layers > 0
+                or r0 ** 3 > (1 << self.log2_table_size))
+
+    def level_resolutions(self) -> list:
+        """Per-level lattice resolution (encoding.py:82-83)."""
+        return [int(round(self.base_resolution * self.growth ** lv)) for lv in range(self.levels)]
+
+    def encoder_widths(self) -> list:
+        return [self.embed_dim] + [self.channels] * self.encoder_layers
+
+    @property
     def latent_resolution(self) -> tuple:
         if self.grid_resolution is not None:
             return self.grid_resolution
@@ -120,20 +141,36 @@ class ModelSpec:
 
     def check_gpu_supported(self) -> None:
         """Raise ConfigError if the spec is outside the GPU kernels' envelope."""
-        if self.encoder_layers != 0:
-            raise ConfigError("encoder MLPs (encoder_layers > 0) are not on the GPU path yet "
-                              "(SURVEY row F3)")
-        if self.levels != 1:
-            raise ConfigError("multi-level hash grids are not on the GPU path yet (SURVEY row F3)")
-        if self.grid_resolution is None:
-            r = self.latent_resolution[0]
-            if r ** 3 > (1 << self.log2_table_size):
-                raise ConfigError("hashed (res^3 > 2^T) levels are not on the GPU path yet")
+        if self.hash_grid:
+            if self.precision != "fp32":
+                raise ConfigError("HashGrid / encoder models run on the exact fp32 path "
+                                  "(precision='fp32'); the tcgen05 kernel needs the dense grid")
+            if self.levels > N.NDF_MAX_LEVELS or self.levels * self.features_per_level > 64:
+                raise ConfigError("HashGrid exceeds the kernel envelope (<= 16 levels, "
+                                  "levels x features <= 64)")
+            if not 1 <= self.log2_table_size < 31:
+                raise ConfigError("log2_table_size must be in [1, 31)")
+            if min(self.level_resolutions()) < 2:
+                raise ConfigError("level resolution must be >= 2")
+            ew = self.encoder_widths()
+            if len(ew) - 1 > N.NDF_MAX_LAYERS or max(ew) > N.NDF_MAX_WIDTH:
+                raise ConfigError("encoder exceeds the kernel envelope (<= 8 layers, width <= 256)")
         widths = self.decoder_widths()
         if len(widths) - 1 > N.NDF_MAX_LAYERS or max(widths) > N.NDF_MAX_WIDTH:
             raise ConfigError("decoder exceeds the kernel envelope (<= 8 layers, width <= 256)")
         if self.fourier_octaves > 12 or self.features_per_level > 64:
             raise ConfigError("encoder exceeds the kernel envelope (L <= 12, C <= 64)")
+
+    @classmethod
+    def reference_default(cls, **kw) -> "ModelSpec":
+        """The reference's ModelSpec() default (model.py:29-46): 6-level HashGrid,
+        4-layer SnakeAlt encoders and decoder, 32 channels, multiply merge, linear head."""
+        fields = dict(merge="multiply", fourier_octaves=4, levels=6, base_resolution=16,
+                      growth=2.0, log2_table_size=16, features_per_level=2, encoder_layers=4,
+                      decoder_layers=4, channels=32, activation="snake_alt", head="linear",
+                      precision="fp32")
+        fields.update(kw)
+        return cls(**fields)
 
     @classmethod
     def baseline(cls, dims, factor: int, measure_kind: str = "pearson",
@@ -147,14 +184,29 @@ class NdfModel:
     """Instantiated NDF (model.py:105-142): host parameters + cached device state."""
 
     def __init__(self, spec: ModelSpec, grid_mu: np.ndarray, grid_nu: np.ndarray,
-                 weights: list, biases: list):
-        rx, ry, rz = spec.latent_resolution
+                 weights: list, biases: list, enc_mu=None, enc_nu=None):
         C = spec.features_per_level
         if spec.shared and grid_mu is not grid_nu:
             raise ConfigError("shared spec requires aliased grids")
+        gshape = self.grid_shape(spec)
         for g in (grid_mu, grid_nu):
-            if g.shape != (rz, ry, rx, C):
-                raise ShapeError(f"latent grid shape {g.shape}, expected {(rz, ry, rx, C)}")
+            if g.shape != gshape:
+                raise ShapeError(f"latent grid shape {g.shape}, expected {gshape}")
+        # encoders: (weights, biases) per branch; identity when encoder_layers == 0
+        enc_mu = enc_mu if enc_mu is not None else ([], [])
+        enc_nu = enc_nu if enc_nu is not None else enc_mu
+        if spec.shared and enc_mu is not enc_nu:
+            raise ConfigError("shared spec requires aliased encoders")
+        ew = spec.encoder_widths()
+        for ews, ebs in (enc_mu, enc_nu):
+            if len(ews) != spec.encoder_layers or len(ebs) != len(ews):
+                raise ConfigError("encoder layer count does not match spec")
+            for i, (w, b) in enumerate(zip(ews, ebs)):
+                if w.shape != (ew[i], ew[i + 1]) or b.shape != (ew[i + 1],):
+                    raise ShapeError(f"encoder layer {i}: weight {w.shape} / bias {b.shape}")
+        self.enc_mu = enc_mu
+        self.enc_nu = enc_nu
+        del C
         widths = spec.decoder_widths()
         if len(weights) != len(widths) - 1 or len(biases) != len(weights):
             raise ConfigError("decoder layer count does not match spec")
@@ -168,22 +220,40 @@ class NdfModel:
         self.biases = biases
         self._dev = {}
 
+    @staticmethod
+    def grid_shape(spec: ModelSpec) -> tuple:
+        """Latent array shape: (levels, 2^T, F) HashGrid tables for the reference family
+        (encoding.py:127-133), (rz, ry, rx, C) for the dense level."""
+        if spec.hash_grid:
+            return (spec.levels, 1 << spec.log2_table_size, spec.features_per_level)
+        rx, ry, rz = spec.latent_resolution
+        return (rz, ry, rx, spec.features_per_level)
+
     @classmethod
     def build(cls, spec: ModelSpec, seed: int = 0, dtype=np.float32) -> "NdfModel":
-        """Seeded init in the reference's RNG order (model.py:131-142; nn.py:76-93)."""
+        """Seeded init in the reference's RNG order (model.py:131-142; nn.py:76-93):
+        grid_mu, enc_mu, [grid_nu, enc_nu], decoder; Kaiming-uniform weights, zero biases."""
         rng = np.random.default_rng(seed)
-        rx, ry, rz = spec.latent_resolution
-        C = spec.features_per_level
         s = spec.grid_init
-        grid_mu = rng.uniform(-s, s, size=(rz, ry, rx, C)).astype(dtype)
-        grid_nu = grid_mu if spec.shared else rng.uniform(-s, s, size=(rz, ry, rx, C)).astype(dtype)
-        widths = spec.decoder_widths()
-        ws, bs = [], []
-        for fan_in, fan_out in zip(widths[:-1], widths[1:]):
-            bound = np.sqrt(6.0 / fan_in)
-            ws.append(rng.uniform(-bound, bound, (fan_in, fan_out)).astype(dtype))
-            bs.append(np.zeros(fan_out, dtype=dtype))
-        return cls(spec, grid_mu, grid_nu, ws, bs)
+        gshape = cls.grid_shape(spec)
+
+        def mlp(widths):
+            ws, bs = [], []
+            for fan_in, fan_out in zip(widths[:-1], widths[1:]):
+                bound = np.sqrt(6.0 / fan_in)
+                ws.append(rng.uniform(-bound, bound, (fan_in, fan_out)).astype(dtype))
+                bs.append(np.zeros(fan_out, dtype=dtype))
+            return ws, bs
+
+        grid_mu = rng.uniform(-s, s, size=gshape).astype(dtype)
+        enc_mu = mlp(spec.encoder_widths())
+        if spec.shared:
+            grid_nu, enc_nu = grid_mu, enc_mu
+        else:
+            grid_nu = rng.uniform(-s, s, size=gshape).astype(dtype)
+            enc_nu = mlp(spec.encoder_widths())
+        ws, bs = mlp(spec.decoder_widths())
+        return cls(spec, grid_mu, grid_nu, ws, bs, enc_mu, enc_nu)
 
     # -- parameters ---------------------------------------------------------
 
@@ -192,6 +262,9 @@ class NdfModel:
         params = [self.grid_mu]
         if not self.spec.shared:
             params.append(self.grid_nu)
+        for enc in ((self.enc_mu,) if self.spec.shared else (self.enc_mu, self.enc_nu)):
+            for w, b in zip(*enc):
+                params.extend((w, b))
         for w, b in zip(self.weights, self.biases):
             params.extend((w, b))
         return params
@@ -211,7 +284,7 @@ class NdfModel:
     def with_precision(self, precision: str) -> "NdfModel":
         """Same parameters, other query precision (shares host arrays)."""
         return NdfModel(replace(self.spec, precision=precision), self.grid_mu, self.grid_nu,
-                        self.weights, self.biases)
+                        self.weights, self.biases, self.enc_mu, self.enc_nu)
 
     # -- device state -------------------------------------------------------
 
@@ -275,15 +348,32 @@ class DeviceModel:
         self.grid_mu = torch.from_numpy(np.ascontiguousarray(model.grid_mu, np.float32)).to(device)
         self.grid_nu = self.grid_mu if spec.shared else torch.from_numpy(
             np.ascontiguousarray(model.grid_nu, np.float32)).to(device)
-        flat = np.concatenate([np.concatenate([w.ravel(), b.ravel()])
-                               for w, b in zip(model.weights, model.biases)]).astype(np.float32)
-        self.params = torch.from_numpy(flat).to(device)
+        def flat(ws, bs):
+            return np.concatenate([np.concatenate([w.ravel(), b.ravel()])
+                                   for w, b in zip(ws, bs)]).astype(np.float32)
+
+        self.params = torch.from_numpy(flat(model.weights, model.biases)).to(device)
         widths = spec.decoder_widths()
         d = N.ModelDesc()
         d.fourier_octaves = spec.fourier_octaves
         d.grid_channels = spec.features_per_level
         for i, r in enumerate(spec.latent_resolution):
             d.grid_res[i] = r
+        self.enc_mu = self.enc_nu = None
+        if spec.hash_grid:
+            d.grid_levels = spec.levels
+            d.grid_log2_table = spec.log2_table_size
+            for i, r in enumerate(spec.level_resolutions()):
+                d.grid_level_res[i] = r
+            d.enc_layers = spec.encoder_layers
+            for i, w in enumerate(spec.encoder_widths()):
+                d.enc_widths[i] = w
+            if spec.encoder_layers:
+                self.enc_mu = torch.from_numpy(flat(*model.enc_mu)).to(device)
+                self.enc_nu = self.enc_mu if spec.shared else torch.from_numpy(
+                    flat(*model.enc_nu)).to(device)
+                d.enc_mu = self.enc_mu.data_ptr()
+                d.enc_nu = self.enc_nu.data_ptr()
         d.merge = N.MERGE[spec.merge]
         d.activation = N.ACT[spec.activation]
         d.head = N.HEAD[spec.head_kind]
@@ -316,8 +406,8 @@ def save_model(model: NdfModel, path) -> None:
     spec = model.spec
     header = dict(asdict(spec))
     header["shared_encoder"] = spec.shared
-    header["grid_resolution"] = list(spec.latent_resolution)
-    header["encoder_widths"] = [spec.embed_dim]
+    header["grid_resolution"] = None if spec.hash_grid else list(spec.latent_resolution)
+    header["encoder_widths"] = spec.encoder_widths()
     header["decoder_widths"] = spec.decoder_widths()
     raw_header = json.dumps(header, sort_keys=True).encode("utf-8")
     with open(path, "wb") as fh:
@@ -329,13 +419,14 @@ def save_model(model: NdfModel, path) -> None:
 
 
 def load_model(path) -> NdfModel:
-    """Read an NDFM container (ours, or a reference one inside the GPU envelope).
+    """Read an NDFM container (ours, or an unmodified reference one, model.py:331-387).
 
-    Reference files (no ``grid_resolution`` key) store the hash table as
-    (levels, 2^T, F); with levels == 1 and a dense level (res^3 <= 2^T) the
-    first res^3 rows are the dense grid in ix + res*(iy + res*iz) order
-    (encoding.py:97-98), and the decoder uses SnakeAlt with a linear output
-    (model.py:141, nn.py:136).
+    Reference files (no ``grid_resolution`` key) store the hash tables as
+    (levels, 2^T, F), then the encoder(s), then the decoder, all SnakeAlt with a
+    linear output (model.py:131-142, nn.py:136).  The reference family loads as
+    is (HashGrid + encoders, exact fp32 path); a single dense level without
+    encoder is converted to the dense layout: its first res^3 rows are the grid
+    in ix + res*(iy + res*iz) order (encoding.py:97-98).
     """
     with open(path, "rb") as fh:
         magic = fh.read(4)
@@ -363,8 +454,6 @@ def load_model(path) -> NdfModel:
     if fields.get("grid_resolution") is not None:
         fields["grid_resolution"] = tuple(fields["grid_resolution"])
     spec = ModelSpec(**fields)
-    if spec.encoder_layers != 0 or spec.levels != 1:
-        raise ConfigError("NDFM model uses encoder MLPs / multi-level grids: not on the GPU path")
     cursor = 0
 
     def take(shape):
@@ -376,24 +465,31 @@ def load_model(path) -> NdfModel:
         cursor += n
         return out
 
+    def take_mlp(widths):
+        ws, bs = [], []
+        for fan_in, fan_out in zip(widths[:-1], widths[1:]):
+            ws.append(take((fan_in, fan_out)))
+            bs.append(take((fan_out,)))
+        return ws, bs
+
     rx, ry, rz = spec.latent_resolution
     C = spec.features_per_level
-    if reference_file:
+    if spec.hash_grid:
+        gshape = NdfModel.grid_shape(spec)
+        t_mu = take(gshape)
+        t_nu = t_mu if spec.shared else take(gshape)
+    elif reference_file:
         T = 1 << spec.log2_table_size
-        if rx ** 3 > T:
-            raise ConfigError("reference NDFM uses a hashed level: not on the GPU path")
         t_mu = take((1, T, C))[0][: rx ** 3].reshape(rz, ry, rx, C).copy()
         t_nu = t_mu if spec.shared else take((1, T, C))[0][: rx ** 3].reshape(rz, ry, rx, C).copy()
     else:
         t_mu = take((rz, ry, rx, C))
         t_nu = t_mu if spec.shared else take((rz, ry, rx, C))
-    widths = spec.decoder_widths()
-    ws, bs = [], []
-    for fan_in, fan_out in zip(widths[:-1], widths[1:]):
-        ws.append(take((fan_in, fan_out)))
-        bs.append(take((fan_out,)))
+    enc_mu = take_mlp(spec.encoder_widths())
+    enc_nu = enc_mu if spec.shared else take_mlp(spec.encoder_widths())
+    ws, bs = take_mlp(spec.decoder_widths())
     if cursor != values.size:
         raise FormatError(f"NDFM payload has {values.size - cursor} stray values")
-    model = NdfModel(spec, t_mu, t_nu, ws, bs)
+    model = NdfModel(spec, t_mu, t_nu, ws, bs, enc_mu, enc_nu)
     model.validate_finite()
     return model

@@ -18,6 +18,12 @@ Fixtures (all inputs seeded, outputs produced by the reference itself):
                      encoder-less, single-dense-level NdfModel with add /
                      absdiff / multiply merges (model.py:279-286): the
                      "reference mode" the GPU kernels must reproduce.
+* ``ndf_refdefault.npz`` the reference's own architecture:
+                     multi-level HashGrid with dense and hashed levels, encoder
+                     MLPs, multiply / concat / add (two-branch) merges, SnakeAlt,
+                     linear head -- parameters + reconstruct_field / forward
+                     outputs; plus the default ModelSpec() built from seed 0
+                     (parameter checksums and outputs).
 * ``pearson.npz``    pearson / pearson_against / pearson_rowwise and
                      ground_truth_field(pearson) (measures.py:59-133, 273-295).
 * ``ksg.npz``        ksg_mi (measures.py:173-203) on seeded vectors incl.
@@ -107,6 +113,49 @@ def main():
         arrays[f"{merge}_p2"] = p2
         arrays[f"{merge}_fwd"] = model.forward(p1, p2)
     np.savez_compressed(os.path.join(HERE, "ndf_refmode.npz"), **arrays)
+
+    # -- reference default family: HashGrid + encoder MLPs -------------
+    arrays = {}
+    dims = (9, 7, 5)
+    arrays["dims"] = np.array(dims)
+    arrays["refs"] = refs
+    p1 = np.random.default_rng(20).uniform(-1.05, 1.05, (40, 3))
+    p2 = np.random.default_rng(21).uniform(-1.05, 1.05, (40, 3))
+    arrays["p1"], arrays["p2"] = p1, p2
+    small = dict(levels=3, base_resolution=4, growth=2.0, log2_table_size=10,
+                 features_per_level=2, encoder_layers=2, decoder_layers=3, channels=16,
+                 fourier_octaves=4)      # res 4, 8 dense; 16^3 > 2^10 hashed
+    cases = [("mul", dict(merge="multiply")), ("cat", dict(merge="concat")),
+             ("add2", dict(merge="add", var_mu="a", var_nu="b"))]
+    for name, extra in cases:
+        spec = ModelSpec(**small, **extra)
+        model = NdfModel.build(spec, seed=31)
+        r = np.random.default_rng(32)
+        grids = [model.grid_mu] if spec.shared else [model.grid_mu, model.grid_nu]
+        for g in grids:          # O(1) tables so the hash gather is not hidden
+            g.tables[:] = r.uniform(-1, 1, g.tables.shape).astype(np.float32)
+        mlps = [model.enc_mu, model.decoder] if spec.shared else \
+            [model.enc_mu, model.enc_nu, model.decoder]
+        for mlp in mlps:
+            for b in mlp.biases:
+                b[:] = r.uniform(-0.2, 0.2, b.shape).astype(np.float32)
+        for i, prm in enumerate(model.parameters()):
+            arrays[f"{name}_param{i}"] = prm
+        arrays[f"{name}_nparams"] = np.array(len(model.parameters()))
+        for k, ref in enumerate(refs):
+            arrays[f"{name}_out{k}"] = reconstruct_field(model, ref, "reference-is-mu", dims).values
+        arrays[f"{name}_outnu"] = reconstruct_field(model, refs[0], "reference-is-nu", dims).values
+        arrays[f"{name}_fwd"] = model.forward(p1, p2)
+    # the unmodified default ModelSpec(): parameters regenerated from the seed (checked
+    # through per-array sums), outputs of the reference itself
+    model = NdfModel.build(ModelSpec(), seed=0)
+    arrays["default_param_sums"] = np.array([float(np.sum(p, dtype=np.float64))
+                                             for p in model.parameters()])
+    arrays["default_param_first"] = np.array([float(p.ravel()[0]) for p in model.parameters()])
+    for k, ref in enumerate(refs):
+        arrays[f"default_out{k}"] = reconstruct_field(model, ref, "reference-is-mu", dims).values
+    arrays["default_fwd"] = model.forward(p1, p2)
+    np.savez_compressed(os.path.join(HERE, "ndf_refdefault.npz"), **arrays)
 
     # -- Pearson --------------------------------------------------------------
     arrays = {}

@@ -216,3 +216,38 @@ def test_large_grid_bf16_vs_fp32():
     idx = np.random.default_rng(5).integers(0, a.numel(), 2000)
     want = O.reconstruct_field(oracle_model(model), ref, dims, vertices=idx)
     assert np.max(np.abs(a.cpu().numpy()[idx] - want)) <= TOL32
+
+
+@pytest.mark.parametrize("case", ["mul", "cat", "add2"])
+def test_reference_default_family_golden(golden, case):
+    """The reference's own architecture (multi-level HashGrid with dense and hashed
+    levels, encoder MLPs, SnakeAlt, linear head) on the exact fp32 path
+    reproduces the unmodified reference's reconstruct_field / forward outputs."""
+    import refdefault as R
+    g = golden("ndf_refdefault")
+    model = R.golden_case(g, case)
+    dims = tuple(int(x) for x in g["dims"])
+    for k, ref in enumerate(g["refs"]):
+        got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
+        assert np.max(np.abs(got - g[f"{case}_out{k}"])) <= 1e-5
+    got = ndf.reconstruct_field(model, g["refs"][0], ndf.ROLE_NU, dims).values
+    assert np.max(np.abs(got - g[f"{case}_outnu"])) <= 1e-5
+    fwd = model.forward(g["p1"], g["p2"])
+    assert np.max(np.abs(fwd - g[f"{case}_fwd"])) <= 1e-5
+    # grid query == points query on the grid nodes, bitwise (same kernels, same order)
+    pos = O.grid_positions(dims)[:64]
+    ref = np.asarray(g["refs"][1]).reshape(1, 3)
+    grid_vals = ndf.reconstruct_field(model, g["refs"][1], ndf.ROLE_MU, dims).values[:64]
+    assert np.array_equal(model.forward(ref, pos), grid_vals)
+
+
+def test_reference_default_model_golden(golden):
+    """ModelSpec() of the reference (6 levels, 2^16-row tables, 4-layer encoders and
+    decoder, 32 channels, multiply merge) built from seed 0 matches the reference."""
+    g = golden("ndf_refdefault")
+    model = ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=0)
+    dims = tuple(int(x) for x in g["dims"])
+    for k, ref in enumerate(g["refs"]):
+        got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
+        assert np.max(np.abs(got - g[f"default_out{k}"])) <= 1e-5
+    assert np.max(np.abs(model.forward(g["p1"], g["p2"]) - g["default_fwd"])) <= 1e-5

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES), set(syms) ^ set(N.SIGNATURES)
-    assert lib.ndf_abi_version() == 1
+    assert lib.ndf_abi_version() == N.NDF_ABI_VERSION == 2
 
 
 def test_status_mapping():
@@ -80,8 +80,13 @@ def test_modelspec_baseline_shapes():
     assert ndf.ModelSpec(measure_kind="ksg_mi").head_kind == "softplus"
     with pytest.raises(ndf.ConfigError):
         ndf.ModelSpec(merge="average")
+    # reference family (encoders / HashGrid): exact fp32 path only
+    ndf.ModelSpec(encoder_layers=2).check_gpu_supported()
+    ndf.ModelSpec.reference_default().check_gpu_supported()
     with pytest.raises(ndf.ConfigError):
-        ndf.ModelSpec(encoder_layers=2).check_gpu_supported()
+        ndf.ModelSpec(encoder_layers=2, precision="fp16").check_gpu_supported()
+    with pytest.raises(ndf.ConfigError):
+        ndf.ModelSpec.reference_default(levels=17).check_gpu_supported()
     with pytest.raises(ndf.ConfigError):
         ndf.ModelSpec(var_mu="a", var_nu="b", shared_encoder=True)
 
@@ -220,3 +225,62 @@ def test_workload_pairs_and_refs():
         assert d.max() <= 16
     refs = W.reference_vertices(W.CONFIGS[3])
     assert refs.shape == (64,)
+
+
+def test_reference_default_build_matches_reference_rng(golden):
+    """NdfModel.build(reference default, seed) draws the reference's parameters
+    (model.py:131-142): per-array sums / first elements from the golden fixture, and
+    bit-for-bit against the importable reference where it exists (build container)."""
+    g = golden("ndf_refdefault")
+    m = ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=0)
+    params = m.parameters()
+    assert len(params) == len(g["default_param_sums"])
+    for p, s, f in zip(params, g["default_param_sums"], g["default_param_first"]):
+        assert float(np.sum(p, dtype=np.float64)) == s
+        assert float(p.ravel()[0]) == f
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        return
+    import sys
+    sys.path.insert(0, ref_src)
+    try:
+        from ndf.model import ModelSpec as RefSpec, NdfModel as RefModel
+    finally:
+        sys.path.remove(ref_src)
+    r = RefModel.build(RefSpec(), seed=0)
+    for a, b in zip(params, r.parameters()):
+        assert np.array_equal(a, b)
+
+
+def test_reference_ndfm_with_hashgrid_and_encoders(tmp_path, golden):
+    """An NDFM written in the reference layout for its default family (HashGrid tables,
+    encoders, decoder) loads unchanged and round-trips through save_model."""
+    import json
+    import struct
+    import refdefault as R
+    g = golden("ndf_refdefault")
+    m = R.golden_case(g, "add2")
+    spec = m.spec
+    header = {k: getattr(spec, k) for k in ("var_mu", "var_nu", "measure_kind", "merge",
+                                             "fourier_octaves", "levels", "base_resolution",
+                                             "growth", "log2_table_size", "features_per_level",
+                                             "encoder_layers", "decoder_layers", "channels")}
+    header.update(shared_encoder=spec.shared, encoder_widths=spec.encoder_widths(),
+                  decoder_widths=spec.decoder_widths())
+    raw = json.dumps(header, sort_keys=True).encode()
+    p = tmp_path / "ref.ndfm"
+    with open(p, "wb") as fh:
+        fh.write(b"NDFM" + struct.pack("<2I", 1, len(raw)) + raw)
+        for a in m.parameters():
+            fh.write(np.ascontiguousarray(a, "<f4").tobytes())
+    m2 = ndf.load_model(p)
+    assert m2.spec.hash_grid and m2.spec.activation == "snake_alt" and m2.spec.head_kind == "linear"
+    assert len(m2.parameters()) == len(m.parameters())
+    for a, b in zip(m.parameters(), m2.parameters()):
+        assert np.array_equal(a, b)
+    q = tmp_path / "ours.ndfm"
+    ndf.save_model(m2, q)
+    m3 = ndf.load_model(q)
+    assert m3.spec == m2.spec
+    for a, b in zip(m2.parameters(), m3.parameters()):
+        assert np.array_equal(a, b)
