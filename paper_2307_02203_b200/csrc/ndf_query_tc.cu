@@ -1008,7 +1008,6 @@ query_pp_kernel(const TcArgs t) {
                      smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid < kC) eref_s[tid] = t.erefs[tid];
   {
     // ones / bias blocks (K-major canonical, SBO 256 B): row r, 8-element group g at
     // (r >> 3) * 256 + g * 128 + (r & 7) * 16; only element k = 0 of each row is nonzero
@@ -1031,6 +1030,12 @@ query_pp_kernel(const TcArgs t) {
     for (int off = 0; off < lay.blob_bytes; off += 32768)
       bulk_g2s(wblob + off, src + off, (uint32_t)min(32768, lay.blob_bytes - off), wbar);
   }
+  // Everything above only touches the model; launched with programmatic stream
+  // serialisation, it overlaps the per-query prep kernels.  Their outputs are read
+  // only after this wait.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid < kC) eref_s[tid] = t.erefs[tid];
+  __syncthreads();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t w_addr = smem_u32(wblob);
   const uint32_t ab_fmt = F16 ? 0u : 1u;
@@ -1296,6 +1301,7 @@ __device__ __forceinline__ void axis_features(double p, float* f) {
 // Same fp64 operations as embed_point_t, so every feature has the same bits; one
 // sincos per thread keeps the fp64 latency chain short.
 __global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_lat, float* lz) {
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nnode = a.nx + a.ny + a.nz + 3;
   const int64_t F = (int64_t)nnode * kL;
@@ -1366,6 +1372,8 @@ __global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_
 template <bool F16>
 __global__ void prep_ws_merge_kernel(const QueryArgs a, const float* __restrict__ feat,
                                      uint32_t* xtab, uint32_t* yztab) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // feat from prep_ws_feat_kernel
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nyz = a.ny * a.nz;
   const int nref = a.nx + a.ny + a.nz;          // first reference node
@@ -1453,6 +1461,25 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
 
 }  // namespace tc
 
+// Launch with programmatic stream serialisation (PDL): the kernel may start while the
+// previous kernel on the stream is still running; it must execute griddepcontrol.wait
+// before consuming that kernel's results.
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static bool tc_supported(const ndf_model_desc& m, std::string* why) {
   auto fail = [&](const char* s) { if (why) *why = s; return false; };
   if (m.grid_levels != 0 || m.enc_layers != 0)
@@ -1509,7 +1536,7 @@ static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid,
     const size_t smem_pp = (size_t)((lay.blob_bytes + 1023) & ~1023) +
                            (size_t)tc::kPPSlots * tc::kABytes +
                            (size_t)(1 + lay.H) * tc::kBiasBlk + 2048;
-    tc::query_pp_kernel<F16, SILU><<<g2, tc::kPPThreads, smem_pp, s>>>(t);
+    NDF_CUDA_CHECK(launch_pdl(tc::query_pp_kernel<F16, SILU>, g2, tc::kPPThreads, smem_pp, s, t));
   }
   NDF_LAUNCH_CHECK();
   return NDF_OK;
@@ -1603,10 +1630,11 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
       tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(a, feat, et, lt);
       NDF_LAUNCH_CHECK();
       const unsigned b2 = (unsigned)((a.nx + nyz + 255) / 256);
+      const float* featc = feat;
       if (a.prec == NDF_PREC_FP16)
-        tc::prep_ws_merge_kernel<true><<<b2, 256, 0, s>>>(a, feat, xt, yt);
+        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<true>, b2, 256, 0, s, a, featc, xt, yt));
       else
-        tc::prep_ws_merge_kernel<false><<<b2, 256, 0, s>>>(a, feat, xt, yt);
+        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<false>, b2, 256, 0, s, a, featc, xt, yt));
       NDF_LAUNCH_CHECK();
     } else {
       const int naxis = a.nx + a.ny + a.nz;
