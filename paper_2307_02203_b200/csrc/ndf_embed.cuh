@@ -73,31 +73,41 @@ __device__ __forceinline__ int64_t hash_row(int res, int log2T, int ix, int iy, 
 
 // Write the fp32 embedding of position (px, py, pz) into out[0..E) via a
 // functor store(idx, value) so callers can target registers, SMEM or global.
+// `part` / `nparts` split the work of one point across cooperating threads (each
+// writes a disjoint set of features, same arithmetic): part 0 does the raw and
+// Fourier features, parts 1.. the latent levels round-robin.  part < 0: everything.
 template <class Store>
 __device__ __forceinline__ void embed_point(const EmbedGeom& g, const float* __restrict__ grid,
-                                            double px, double py, double pz, Store store) {
+                                            double px, double py, double pz, Store store,
+                                            int part = -1, int nparts = 1) {
   const double p[3] = {fmin(fmax(px, -1.0), 1.0), fmin(fmax(py, -1.0), 1.0),
                        fmin(fmax(pz, -1.0), 1.0)};
-  store(0, (float)p[0]);
-  store(1, (float)p[1]);
-  store(2, (float)p[2]);
-  double scale = 3.141592653589793;   // 2^i * pi, exact doubling
-  for (int i = 0; i < g.L; ++i) {
+  const bool all = part < 0;
+  if (all || part == 0) {
+    store(0, (float)p[0]);
+    store(1, (float)p[1]);
+    store(2, (float)p[2]);
+    double scale = 3.141592653589793;   // 2^i * pi, exact doubling
+    for (int i = 0; i < g.L; ++i) {
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      double s, c;
-      sincos(dmul(scale, p[ax]), &s, &c);
-      store(3 + 6 * i + 2 * ax, (float)s);
-      store(3 + 6 * i + 2 * ax + 1, (float)c);
+      for (int ax = 0; ax < 3; ++ax) {
+        double s, c;
+        sincos(dmul(scale, p[ax]), &s, &c);
+        store(3 + 6 * i + 2 * ax, (float)s);
+        store(3 + 6 * i + 2 * ax + 1, (float)c);
+      }
+      scale = scale * 2.0;
     }
-    scale = scale * 2.0;
   }
+  const int lstep = all ? 1 : (nparts > 1 ? nparts - 1 : 1);
+  const int lfirst = all ? 0 : (nparts > 1 ? part - 1 : 0);
+  if (!all && nparts > 1 && part == 0) return;
   if (g.levels > 0) {
     // HashGrid (encoding.py:149-178): per level, trilinear over the 8 corners in
     // _CORNER_OFFSETS order, weights ((1*wx)*wy)*wz and the corner sum in fp64,
     // output concatenated coarse to fine.
     const int64_t T = (int64_t)1 << g.log2T;
-    for (int lv = 0; lv < g.levels; ++lv) {
+    for (int lv = lfirst; lv < g.levels; lv += lstep) {
       const int res = g.lres[lv];
       const AxisCoord cx = level_coord(p[0], res);
       const AxisCoord cy = level_coord(p[1], res);
@@ -125,6 +135,7 @@ __device__ __forceinline__ void embed_point(const EmbedGeom& g, const float* __r
     }
     return;
   }
+  if (lfirst != 0) return;          // the single dense level belongs to part 1
   const AxisCoord cx = level_coord(p[0], g.rx);
   const AxisCoord cy = level_coord(p[1], g.ry);
   const AxisCoord cz = level_coord(p[2], g.rz);

@@ -28,17 +28,24 @@ __device__ __forceinline__ int enc_out_dim(const ndf_model_desc& m, int E) {
 
 // One dense layer over the tile: Hout[j][v] = act(sum_k Hin[k][v] W[k][j] + b[j]) for
 // j < N (sequential ascending k, unfused fp32 -- matmul_exact); `act` false = linear.
-__device__ __forceinline__ void tile_layer(const float* Hin, float* Hout, const float* W,
-                                           const float* b, int K, int N, bool act, int kind) {
-  for (int j = threadIdx.x; j < N; j += kThreadsF32) {
-    float acc[kTV];
+// Narrow layers split the tile's vertices across thread groups (VPT vertices per
+// thread) so all 128 threads work; every output keeps the same arithmetic order.
+template <int VPT>
+__device__ __forceinline__ void tile_layer_v(const float* Hin, float* Hout, const float* W,
+                                             const float* b, int K, int N, bool act, int kind) {
+  constexpr int kGroups = kTV / VPT;
+  constexpr int kJT = kThreadsF32 / kGroups;      // threads per vertex group
+  const int grp = threadIdx.x / kJT;
+  const int v0 = grp * VPT;
+  for (int j = threadIdx.x % kJT; j < N; j += kJT) {
+    float acc[VPT];
 #pragma unroll
-    for (int v = 0; v < kTV; ++v) acc[v] = 0.0f;
+    for (int v = 0; v < VPT; ++v) acc[v] = 0.0f;
     for (int k = 0; k < K; ++k) {
       const float w = __ldg(W + (size_t)k * N + j);
-      const float4* hr = reinterpret_cast<const float4*>(Hin + k * kTVP);
+      const float4* hr = reinterpret_cast<const float4*>(Hin + k * kTVP + v0);
 #pragma unroll
-      for (int q = 0; q < kTV / 4; ++q) {
+      for (int q = 0; q < VPT / 4; ++q) {
         const float4 h = hr[q];
         acc[4 * q + 0] = fadd(acc[4 * q + 0], fmul(h.x, w));
         acc[4 * q + 1] = fadd(acc[4 * q + 1], fmul(h.y, w));
@@ -47,9 +54,9 @@ __device__ __forceinline__ void tile_layer(const float* Hin, float* Hout, const 
       }
     }
     const float bj = __ldg(b + j);
-    float4* ho = reinterpret_cast<float4*>(Hout + j * kTVP);
+    float4* ho = reinterpret_cast<float4*>(Hout + j * kTVP + v0);
 #pragma unroll
-    for (int q = 0; q < kTV / 4; ++q) {
+    for (int q = 0; q < VPT / 4; ++q) {
       float o[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -60,6 +67,13 @@ __device__ __forceinline__ void tile_layer(const float* Hin, float* Hout, const 
     }
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void tile_layer(const float* Hin, float* Hout, const float* W,
+                                           const float* b, int K, int N, bool act, int kind) {
+  if (N <= kThreadsF32 / 4) tile_layer_v<kTV / 4>(Hin, Hout, W, b, K, N, act, kind);
+  else if (N <= kThreadsF32 / 2) tile_layer_v<kTV / 2>(Hin, Hout, W, b, K, N, act, kind);
+  else tile_layer_v<kTV>(Hin, Hout, W, b, K, N, act, kind);
 }
 
 // Encoder MLP over the tile (Mlp.forward, nn.py:124-137): activation on all layers
@@ -151,24 +165,25 @@ query_f32_kernel(const QueryArgs a) {
   for (int64_t tile = blockIdx.x; tile * kTV < n_vert; tile += gridDim.x) {
     const int64_t base = a.v0 + tile * kTV;
     const int nv = (int)min((int64_t)kTV, a.v1 - base);
-    // ---- embed: one thread per vertex, written k-major into column v ------------
-    if (tid < kTV) {
-      const int v = tid;
+    // ---- embed: 4 threads per vertex (Fourier | latent levels), k-major column v --
+    {
+      const int v = tid % kTV, part = tid / kTV;
       if (v < nv) {
         const int64_t gv = base + v;
         if (a.mode == 0) {
           double p[3];
           vertex_position(a, gv, p);
           const float* grid = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
-          embed_point(g, grid, p[0], p[1], p[2], [&](int i, float x) { B0[i * kTVP + v] = x; });
+          embed_point(g, grid, p[0], p[1], p[2], [&](int i, float x) { B0[i * kTVP + v] = x; },
+                      part, kThreadsF32 / kTV);
         } else {
           const int64_t im = a.n_mu == 1 ? 0 : gv;
           embed_point(g, a.m.grid_mu, a.p_mu[3 * im], a.p_mu[3 * im + 1], a.p_mu[3 * im + 2],
-                      [&](int i, float x) { B2[i * kTVP + v] = x; });
+                      [&](int i, float x) { B2[i * kTVP + v] = x; }, part, kThreadsF32 / kTV);
           embed_point(g, a.m.grid_nu, a.p_nu[3 * gv], a.p_nu[3 * gv + 1], a.p_nu[3 * gv + 2],
-                      [&](int i, float x) { B0[i * kTVP + v] = x; });
+                      [&](int i, float x) { B0[i * kTVP + v] = x; }, part, kThreadsF32 / kTV);
         }
-      } else {
+      } else if (part == 0) {
         for (int i = 0; i < E; ++i) {
           B0[i * kTVP + v] = 0.0f;
           if (a.mode == 1) B2[i * kTVP + v] = 0.0f;
