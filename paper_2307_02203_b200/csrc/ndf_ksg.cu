@@ -227,9 +227,10 @@ __device__ __forceinline__ double knn_scan(const double* __restrict__ sx,
     const int j = left ? l : r;
     const double d = fmax(dx, fabs(dsub(yi, yx[j])));
     if (d < top[KP1 - 1]) {
+      // sorted insert; top[0] is the point itself (distance 0 <= d) and never moves
 #pragma unroll
-      for (int s = KP1 - 1; s > 0; --s) top[s] = d < top[s - 1] ? top[s - 1] : fmin(d, top[s]);
-      top[0] = fmin(d, top[0]);
+      for (int s = KP1 - 1; s > 1; --s) top[s] = d < top[s - 1] ? top[s - 1] : fmin(d, top[s]);
+      top[1] = fmin(d, top[1]);
     }
     if (left) { --l; dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY; }
     else { ++r; dr = r < M ? dsub(sx[r], xi) : INFINITY; }
