@@ -119,11 +119,57 @@ def dense_grid_encode(positions, table):
     return np.einsum("mc,mcf->mf", w, feats, optimize=False)
 
 
+HASH_PRIMES = (np.uint64(1), np.uint64(2654435761), np.uint64(805459861))   # encoding.py:17
+
+
+@dataclass
+class HashGridSpec:
+    """The reference HashGrid (encoding.py:55-86): tables (levels, 2^T, F)."""
+
+    tables: np.ndarray
+    level_res: tuple          # round(base * growth^l) (encoding.py:82-83)
+    log2_table: int
+
+
+def hash_grid_encode(positions, grid: HashGridSpec):
+    """HashGrid.encode (encoding.py:163-178) via _level_lookup (:149-161): per level,
+    level_coords, corner rows dense (res^3 <= 2^T) or XOR-prime hashed mod 2^T
+    (_corner_indices, :90-102), weights ((1*wx)*wy)*wz, fp64 corner sum."""
+    pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+    levels, T, F = grid.tables.shape
+    out = np.empty((pos.shape[0], levels * F))
+    for lv in range(levels):
+        res = grid.level_res[lv]
+        i0 = np.empty((pos.shape[0], 3), dtype=np.int64)
+        t = np.empty((pos.shape[0], 3))
+        for axis in range(3):
+            i0[:, axis], t[:, axis] = level_coords(pos[:, axis], res)
+        corners = i0[:, None, :] + CORNER_OFFSETS[None, :, :]
+        ix, iy, iz = corners[..., 0], corners[..., 1], corners[..., 2]
+        if res ** 3 <= T:
+            idx = (ix + res * (iy + res * iz)).astype(np.int64)
+        else:
+            h = (ix.astype(np.uint64) * HASH_PRIMES[0] ^ iy.astype(np.uint64) * HASH_PRIMES[1]
+                 ^ iz.astype(np.uint64) * HASH_PRIMES[2])
+            idx = (h & np.uint64(T - 1)).astype(np.int64)
+        w = np.ones(corners.shape[:2])
+        for axis in range(3):
+            frac = t[:, axis:axis + 1]
+            on = CORNER_OFFSETS[:, axis][None, :]
+            w = w * np.where(on, frac, 1.0 - frac)
+        feats = grid.tables[lv].astype(np.float64)[idx]
+        out[:, lv * F:(lv + 1) * F] = np.einsum("mc,mcf->mf", w, feats, optimize=False)
+    return out
+
+
 def embed(positions, table, L):
-    """model.py:169-177 -- [raw | fourier | grid] computed in fp64, cast fp32."""
+    """model.py:169-177 -- [raw | fourier | grid] computed in fp64, cast fp32.
+    ``table``: dense (rz, ry, rx, C) array or a HashGridSpec (reference family)."""
     pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
     clamped = np.clip(pos, -1.0, 1.0)
-    parts = [clamped, fourier_encode(clamped, L), dense_grid_encode(clamped, table)]
+    grid = (hash_grid_encode(clamped, table) if isinstance(table, HashGridSpec)
+            else dense_grid_encode(clamped, table))
+    parts = [clamped, fourier_encode(clamped, L), grid]
     return np.concatenate(parts, axis=1).astype(np.float32)
 
 
@@ -192,21 +238,30 @@ def mlp_forward(weights, biases, act, x):
 
 @dataclass
 class OracleModel:
-    """BASELINE-architecture NDF: dense latent grid(s), no encoder MLP."""
+    """NDF of either family: BASELINE (dense latent grid, no encoder MLP) or the
+    reference's own (HashGridSpec grids + per-branch encoder MLPs, model.py:105-189)."""
 
     L: int
-    grid_mu: np.ndarray          # (rz, ry, rx, C) fp32
-    grid_nu: np.ndarray
-    weights: list = field(default_factory=list)   # (fan_in, fan_out) fp32
+    grid_mu: object              # (rz, ry, rx, C) fp32 array, or HashGridSpec
+    grid_nu: object
+    weights: list = field(default_factory=list)   # decoder (fan_in, fan_out) fp32
     biases: list = field(default_factory=list)
     merge: str = "sum_absdiff"
     act: str = "silu"
     head: str = "tanh"
+    enc_mu: tuple = ((), ())     # encoder (weights, biases); empty = identity (nn.py:84-86)
+    enc_nu: tuple = ((), ())
+
+    def encode(self, positions, grid, enc):
+        """embed, then the branch encoder MLP (model.py:184-185)."""
+        e = embed(positions, grid, self.L)
+        ws, bs = enc
+        return mlp_forward(list(ws), list(bs), self.act, e) if len(ws) else e
 
     def forward(self, p_mu, p_nu):
-        """model.py:179-189 (encoder_layers=0 => identity encoders)."""
-        a = embed(p_mu, self.grid_mu, self.L)
-        b = embed(p_nu, self.grid_nu, self.L)
+        """model.py:179-189."""
+        a = self.encode(p_mu, self.grid_mu, self.enc_mu)
+        b = self.encode(p_nu, self.grid_nu, self.enc_nu)
         if a.shape[0] == 1 and b.shape[0] > 1:
             a = np.broadcast_to(a, b.shape)
         if b.shape[0] == 1 and a.shape[0] > 1:
@@ -262,10 +317,12 @@ def reconstruct_field(model: OracleModel, ref, dims, role="reference-is-mu",
     ref_is_mu = role == "reference-is-mu"
     ref_grid = model.grid_mu if ref_is_mu else model.grid_nu
     query_grid = model.grid_nu if ref_is_mu else model.grid_mu
-    ref_features = embed(ref, ref_grid, model.L)
+    ref_enc = model.enc_mu if ref_is_mu else model.enc_nu
+    query_enc = model.enc_nu if ref_is_mu else model.enc_mu
+    ref_features = model.encode(ref, ref_grid, ref_enc)
     out = np.empty(positions.shape[0], dtype=np.float32)
     for s in range(0, positions.shape[0], batch_size):
-        q = embed(positions[s:s + batch_size], query_grid, model.L)
+        q = model.encode(positions[s:s + batch_size], query_grid, query_enc)
         r = np.broadcast_to(ref_features, q.shape)
         merged = merge(model.merge, r, q) if ref_is_mu else merge(model.merge, q, r)
         z = mlp_forward(model.weights, model.biases, model.act, merged)

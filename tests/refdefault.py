@@ -35,3 +35,18 @@ def golden_case(g, name):
     spec = ndf.ModelSpec(**SMALL, **CASES[name])
     params = [g[f"{name}_param{i}"] for i in range(int(g[f"{name}_nparams"]))]
     return model_from_params(spec, params)
+
+
+def oracle_model(model):
+    """oracle/ndf_oracle.py restatement of an NdfModel (either family)."""
+    from oracle import ndf_oracle as O
+    spec = model.spec
+    if spec.hash_grid:
+        def grid(t):
+            return O.HashGridSpec(t, tuple(spec.level_resolutions()), spec.log2_table_size)
+        g_mu, g_nu = grid(model.grid_mu), grid(model.grid_nu)
+    else:
+        g_mu, g_nu = model.grid_mu, model.grid_nu
+    return O.OracleModel(spec.fourier_octaves, g_mu, g_nu, model.weights, model.biases,
+                         spec.merge, spec.activation, spec.head_kind,
+                         tuple(model.enc_mu), tuple(model.enc_nu))

@@ -251,3 +251,25 @@ def test_reference_default_model_golden(golden):
         got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
         assert np.max(np.abs(got - g[f"default_out{k}"])) <= 1e-5
     assert np.max(np.abs(model.forward(g["p1"], g["p2"]) - g["default_fwd"])) <= 1e-5
+
+
+def test_reference_default_vs_oracle_c0_grid():
+    """Reference default model (seed 7, O(1) tables, random biases) over config 0's grid
+    with an off-node reference: GPU exact path vs the oracle restatement."""
+    import refdefault as R
+    m = ndf.NdfModel.build(ndf.ModelSpec.reference_default(shared_encoder=False, var_mu="a",
+                                                           var_nu="b", merge="concat"), seed=7)
+    r = np.random.default_rng(8)
+    for t in (m.grid_mu, m.grid_nu):
+        t[:] = r.uniform(-1, 1, t.shape).astype(np.float32)
+    for ws, bs in (m.enc_mu, m.enc_nu, (m.weights, m.biases)):
+        for b in bs:
+            b[:] = r.uniform(-0.2, 0.2, b.shape).astype(np.float32)
+    m.invalidate()
+    dims = (32, 44, 4)
+    ref = (0.137, -0.52, 0.91)
+    om = R.oracle_model(m)
+    for role in (ndf.ROLE_MU, ndf.ROLE_NU):
+        got = ndf.reconstruct_field(m, ref, role, dims).values
+        want = O.reconstruct_field(om, ref, dims, role=role)
+        assert np.max(np.abs(got - want)) <= 1e-5

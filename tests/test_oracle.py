@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import ndf_oracle as O
+import paper_2307_02203_b200 as ndf
 
 
 def test_fourier_bitwise(golden):
@@ -140,3 +141,27 @@ def test_ground_truth_ksg_bitwise(golden):
     dims = tuple(int(d) for d in g["gt_dims"])
     out = O.ground_truth_field(g["field"], "ksg_mi", g["gt_ref"], dims, k=int(g["gt_k"]))
     assert np.array_equal(out, g["gt_mi"])
+
+
+@pytest.mark.parametrize("case", ["mul", "cat", "add2"])
+def test_reference_family_restatement_bitwise(golden, case):
+    """oracle HashGrid + encoder restatement == the unmodified reference, bit for bit."""
+    import refdefault as R
+    g = golden("ndf_refdefault")
+    om = R.oracle_model(R.golden_case(g, case))
+    dims = tuple(int(x) for x in g["dims"])
+    for k, ref in enumerate(g["refs"]):
+        assert np.array_equal(O.reconstruct_field(om, ref, dims), g[f"{case}_out{k}"])
+    assert np.array_equal(O.reconstruct_field(om, g["refs"][0], dims, role="reference-is-nu"),
+                          g[f"{case}_outnu"])
+    assert np.array_equal(om.forward(g["p1"], g["p2"]), g[f"{case}_fwd"])
+
+
+def test_reference_default_restatement_bitwise(golden):
+    import refdefault as R
+    g = golden("ndf_refdefault")
+    m = ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=0)
+    om = R.oracle_model(m)
+    dims = tuple(int(x) for x in g["dims"])
+    assert np.array_equal(O.reconstruct_field(om, g["refs"][0], dims), g["default_out0"])
+    assert np.array_equal(om.forward(g["p1"], g["p2"]), g["default_fwd"])
