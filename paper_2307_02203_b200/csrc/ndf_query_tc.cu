@@ -843,13 +843,13 @@ __device__ __forceinline__ void issue_ksteps(uint32_t d_tmem, uint32_t a_addr, u
   }
 }
 // A operand in TMEM ("TS" form): K16 steps [k0, k0 + nsteps), step kk's 8 columns at
-// a_col(kk) = a_tmem + 8 kk + (kk >= 4 ? 32 : 0) (each column half of the epilogue packs
-// its 64 K-values into the first 32 of its own, already drained, 64 columns).
+// a_col(kk) = a_tmem + 32 (kk / 2) + 8 (kk % 2) (the epilogue packs each 32-column
+// K-chunk's 16-bit activations into the first 16 of its own, already drained, columns).
 __device__ __forceinline__ void issue_ksteps_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_addr,
                                                 int k0, int nsteps, uint32_t sbo_b,
                                                 uint32_t idesc, bool accumulate_first) {
   for (int kk = k0; kk < k0 + nsteps; ++kk) {
-    const uint32_t ac = a_tmem + (uint32_t)(8 * kk + (kk >= 4 ? 32 : 0));
+    const uint32_t ac = a_tmem + (uint32_t)(32 * (kk >> 1) + 8 * (kk & 1));
     const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
     const uint32_t acc = (kk > k0 || accumulate_first) ? 1u : 0u;
     asm volatile(
@@ -1117,7 +1117,16 @@ query_pp_kernel(const TcArgs t) {
   } else {
     // ======================== epilogue (slot s, column half ch) ======================
     const int ch = wg & 1;
-    const bool issuer = ch == 0 && wq == 0;        // warp issuing slot s's MMAs
+#ifndef NDF_ISSUER_Q
+#define NDF_ISSUER_Q 0
+#endif
+    const bool issuer = ch == 0 && wq == NDF_ISSUER_Q;   // warp issuing slot s's MMAs
+    // K-chunks (32 columns each) drained by this warp.  The issuer's MMA issue blocks
+    // it for ~70 cycles per K16 step (tools/micro/mma_issue.cu), so it drains only
+    // chunk 0 and its lane-quarter sibling takes chunks 1-3; everyone else drains
+    // half a row (chunks 0-1 or 2-3).  MUFU work per sub-partition is unchanged.
+    const int kc_begin = wq == NDF_ISSUER_Q ? (ch == 0 ? 0 : 1) : 2 * ch;
+    const int kc_end = wq == NDF_ISSUER_Q ? (ch == 0 ? 1 : 4) : 2 * ch + 2;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     mbar_wait(wbar, 0);
     const float bias_out = vecs[H * kHid];
@@ -1128,89 +1137,84 @@ query_pp_kernel(const TcArgs t) {
 #pragma unroll 1
       for (int l = 0; l < H; ++l) {
         const uint32_t half = (uint32_t)((kk * H + l) & 1);
-        const uint32_t d_row = d_slot + lane_base + half * kHid + (uint32_t)(64 * ch);
+        const uint32_t d_base = d_slot + lane_base + half * kHid;   // this lane quarter
         mbar_wait(&acc_full[s], acc_ph);
         acc_ph ^= 1u;
         tc_fence_after();
         if (l == 0 && issuer && lane == 0) mbar_arrive(&s_free[s]);   // SMEM A reusable
         NDF_TRACE_AT((int)kk, 2 * l);
         float va[16], vb[16];
-        tmem_ld16_nowait(d_row, va);
+        tmem_ld16_nowait(d_base + (uint32_t)(32 * kc_begin), va);
         tmem_wait_ld();
+        // debug trace: per-warp stamps of CTA 0, tile 3, layer 1 (tools/trace_ws.py)
+#define NDF_TRACE_WARP(e)                                                                  \
+  if (t.trace && blockIdx.x == 0 && lane == 0 && kk == 3 && l == 1)                      \
+    t.trace[kTraceBase + 16 + warp * 8 + (e)] = clock64();
+        NDF_TRACE_WARP(0);
         if (l + 1 < H) {
-          // ---- hidden layer l -> A of layer l+1 (packed into this warp's drained TMEM
-          // columns), whose MMA follows K-chunk by K-chunk ----------------------------
+          // ---- hidden layer l -> A of layer l+1: K-chunk kc (32 columns) is packed into
+          // the first 16 of its own, just drained, TMEM columns; its two K16 MMA steps of
+          // layer l+1 are issued once the 4 warps owning it have stored it --------------
           const uint32_t d_next = d_slot + (half ^ 1u) * kHid;
           const uint32_t a_tm = d_slot + half * kHid;                  // A of layer l+1
-          const uint32_t a_row = d_row;   // this warp's lanes, its own column half
           const uint32_t wl = w_addr + lay.w0_bytes + l * lay.wh_bytes;
 #pragma unroll 1
-          for (int j = 0; j < 4; j += 2) {            // two 16-column sub-chunks = 1 K-chunk
-            const int c0 = 64 * ch + 16 * j;
-            tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 16), vb);
-            epilogue16<F16, SILU>(va, a.m.activation, a_row + (uint32_t)(8 * j));
+          for (int kc = kc_begin; kc < kc_end; ++kc) {
+            const uint32_t col = (uint32_t)(32 * kc);
+            tmem_ld16_nowait(d_base + col + 16u, vb);
+            epilogue16<F16, SILU>(va, a.m.activation, d_base + col);
             tmem_wait_ld();
-            if (j + 2 < 4) tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 32), va);
-            epilogue16<F16, SILU>(vb, a.m.activation, a_row + (uint32_t)(8 * j + 8));
+            if (kc + 1 < kc_end) tmem_ld16_nowait(d_base + col + 32u, va);
+            epilogue16<F16, SILU>(vb, a.m.activation, d_base + col + 8u);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            NDF_TRACE_WARP(1 + kc);
             tc_fence_before();
-#ifdef NDF_EXP_NOSYNC
-            if (j + 2 < 4) { tmem_wait_ld(); continue; }
-            named_bar(1 + 4 * s, 256);
-            if (issuer && lane == 0) {
-              tc_fence_after();
-              mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),
-                       smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
-              issue_ksteps_ts(d_next, a_tm, wl, 0, 8, kSboA, idesc, true);
-              mma_commit(&acc_full[s]);
-            }
-            continue;
-#endif
-            const int kc = c0 >> 5;                   // K-chunk just completed
-            const int nthr = ch == 0 ? 128 : 160;     // half 1: + the issuing warp
+            // K-chunk barriers: chunk 0's writers include the issuer (128 threads); the
+            // other chunks' 4 writers arrive and the issuer waits (160)
             if (issuer) {
-              if (kc < 2) {
-                named_bar(1 + 4 * s + kc, nthr);
-              }
+              named_bar(1 + 4 * s, 128);
               if (lane == 0) {
                 tc_fence_after();
-                if (kc == 0)                          // D = bias of layer l+1
-                  mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),
-                           smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
-                issue_ksteps_ts(d_next, a_tm, wl, 2 * kc, 2, kSboA, idesc, true);
+                mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
+                         smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+                issue_ksteps_ts(d_next, a_tm, wl, 0, 2, kSboA, idesc, true);
               }
-              if (kc == 1) {                          // then half 1's K-chunks 2, 3
 #pragma unroll 1
-                for (int k2 = 2; k2 < 4; ++k2) {
-                  named_bar(1 + 4 * s + k2, 160);
-                  if (lane == 0) {
-                    tc_fence_after();
-                    issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
-                    if (k2 == 3) mma_commit(&acc_full[s]);
-                  }
+              for (int k2 = 1; k2 < 4; ++k2) {
+                named_bar(1 + 4 * s + k2, 160);
+                if (lane == 0) {
+                  tc_fence_after();
+                  issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+                  if (k2 == 3) mma_commit(&acc_full[s]);
                 }
               }
             } else {
-              named_bar_arrive(1 + 4 * s + kc, nthr);
+              named_bar_arrive(1 + 4 * s + kc, kc == 0 ? 128 : 160);
             }
-            if (j + 2 < 4) tmem_wait_ld();
+            if (kc + 1 < kc_end) tmem_wait_ld();
           }
+          NDF_TRACE_WARP(6);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
         } else {
           // ---- last hidden layer: A is free for the producer; fp32 output dot ---------
           // layer H-1's MMA has completed, so the other D half (which held layer H-2 and
           // then A of layer H-1) is free for the next tile's layer 0
           if (issuer && lane == 0) mbar_arrive(&d_free[s]);
+          // the output dot product always splits at column 64 (the issuer's lane quarter
+          // included), so its fp32 summation order -- and the bits -- never depend on a
+          // vertex's row within the tile
           float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (kc_begin != 2 * ch) tmem_ld16_nowait(d_base + (uint32_t)(64 * ch), va);
+          if (kc_begin != 2 * ch) tmem_wait_ld();
 #pragma unroll 1
-          for (int j = 0; j < 4; j += 2) {
-            const int c0 = 64 * ch + 16 * j;
-            tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 16), vb);
-            dot16<SILU>(va, c0, a.m.activation, wout_addr, dots);
+          for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
+            const int col = 32 * kc;
+            tmem_ld16_nowait(d_base + (uint32_t)(col + 16), vb);
+            dot16<SILU>(va, col, a.m.activation, wout_addr, dots);
             tmem_wait_ld();
-            if (j + 2 < 4) tmem_ld16_nowait(d_row + (uint32_t)(16 * j + 32), va);
-            dot16<SILU>(vb, c0 + 16, a.m.activation, wout_addr, dots);
-            if (j + 2 < 4) tmem_wait_ld();
+            if (kc + 1 < 2 * ch + 2) tmem_ld16_nowait(d_base + (uint32_t)(col + 32), va);
+            dot16<SILU>(vb, col + 16, a.m.activation, wout_addr, dots);
+            if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
           }
           tc_fence_before();
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
@@ -1661,7 +1665,7 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) { return run_tc(a, nullp
 using namespace ndf;
 
 // Debug only (not part of the C-ABI header): subsequent tensor-core queries record
-// CTA 0's per-phase clock64() stamps into buf[6 * 32 * 12 + 16] (NULL disables).
+// CTA 0's per-phase clock64() stamps into buf[6 * 32 * 12 + 16 + 16 * 8] (NULL disables).
 extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 
 extern "C" size_t ndf_tc_blob_bytes(const ndf_model_desc* m) {

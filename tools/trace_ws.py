@@ -70,11 +70,11 @@ if fine:
     f = np.mean(np.array(fine), axis=0)
     print("layer-1 fine (cycles after acc1): ld0 %.0f  sub0 %.0f  st0 %.0f  kc0 %.0f  st1 %.0f  end %.0f" % tuple(f))
 
-# per-warp stamps of tile 3, layer 1 (E-warps 0..15): start, sub0, st0(K-chunk 0), sub2, st1, end
+# per-warp stamps of tile 3, layer 1 (E-warps 0..15): start, K-chunk 0..3 stored, end
 w = buf.cpu().numpy()[6 * 32 * 12 + 16:].reshape(16, 8).astype(np.int64)
 if w[0, 0]:
     base = w[:, 0].min()
     print("per-warp layer-1 stamps (tile 3), cycles after the first warp starts:")
     for i in range(16):
-        print(f"  warp {i:2d} (slot {i // 8}, cols {64 * ((i // 4) % 2)}+)", " ".join(
-            f"{x - base:6d}" for x in w[i, [0, 1, 2, 3, 4, 6]]))
+        print(f"  warp {i:2d} (slot {i // 8}, half {(i // 4) % 2})", " ".join(
+            f"{x - base:6d}" if x else "     -" for x in w[i, [0, 1, 2, 3, 4, 6]]))
