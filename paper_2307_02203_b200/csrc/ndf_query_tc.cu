@@ -748,86 +748,6 @@ query_tc_kernel(const TcArgs t, const int nwg) {
                  "r"(tmem_cols));
 }
 
-// Hidden-layer epilogue of one 32-column chunk: bias (all 8 LDS.128 first), then
-// the 32 independent MUFU tanh back to back, then FMA + 16-bit pack + 4 STS.128.
-// st_shared_v4 carries no "memory" clobber, so the bias loads are free to move
-// ahead of earlier chunks' stores (the A buffer is only read by the tensor cores,
-// after fence.proxy.async).
-template <bool F16, bool SILU>
-__device__ __forceinline__ void epilogue_chunk(const float* v, const float4* b4, int c0,
-                                               int act, uint32_t a_addr, int row) {
-  float x[32];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 b = b4[(c0 >> 2) + q];
-    x[4 * q] = v[4 * q] + b.x;
-    x[4 * q + 1] = v[4 * q + 1] + b.y;
-    x[4 * q + 2] = v[4 * q + 2] + b.z;
-    x[4 * q + 3] = v[4 * q + 3] + b.w;
-  }
-  float h[32];
-  if constexpr (SILU) {       // x = z/2 (weights pre-scaled): silu(z) = x + x*tanh(x)
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = tanh_fast(x[i]);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = fmaf(x[i], h[i], x[i]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = act_f32(act, x[i]);
-  }
-#pragma unroll
-  for (int jj = 0; jj < 4; ++jj)
-    st_shared_v4(a_addr + canon_off(row, c0 + 8 * jj, kSboA), pack2<F16>(h[8 * jj], h[8 * jj + 1]),
-                 pack2<F16>(h[8 * jj + 2], h[8 * jj + 3]), pack2<F16>(h[8 * jj + 4], h[8 * jj + 5]),
-                 pack2<F16>(h[8 * jj + 6], h[8 * jj + 7]));
-}
-
-// Last hidden layer: bias + activation in fp32, then the output layer's dot product
-// (128 -> 1) on the FMA pipe in fp32.  The fp32 output weights live in rows 1-2 of
-// the packed N=16 output operand (whose columns 1..15 nobody reads): k-group g's 8
-// weights are the 32 bytes at g*128 + 16.  Four partial sums break the FMA chain.
-template <bool SILU>
-__device__ __forceinline__ void epilogue_dot(const float* v, const float4* b4, int c0, int act,
-                                             uint32_t wout_addr, float* dots) {
-  float x[32], w[32];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 b = b4[(c0 >> 2) + q];
-    x[4 * q] = v[4 * q] + b.x;
-    x[4 * q + 1] = v[4 * q + 1] + b.y;
-    x[4 * q + 2] = v[4 * q + 2] + b.z;
-    x[4 * q + 3] = v[4 * q + 3] + b.w;
-    const uint32_t wa = wout_addr + (uint32_t)(((c0 >> 3) + (q >> 1)) * 128 + 16 + 16 * (q & 1));
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(w[4 * q]), "=f"(w[4 * q + 1]), "=f"(w[4 * q + 2]), "=f"(w[4 * q + 3]) : "r"(wa));
-  }
-  float h[32];
-  if constexpr (SILU) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = tanh_fast(x[i]);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = fmaf(x[i], h[i], x[i]);   // x = z/2: silu(z)
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) h[i] = act_f32(act, x[i]);
-  }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) dots[i & 3] = fmaf(h[i], w[i], dots[i & 3]);
-}
-
-__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float* v) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
