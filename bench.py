@@ -71,18 +71,58 @@ def load_peaks():
 # clocks sampler (nvidia-smi during the timed region)
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region.
+
+    NVML polled from a thread every ~0.5 ms (the timed region of a default run is only
+    tens of ms), falling back to ``nvidia-smi -lms 50``.  One sample is taken before
+    the region starts and one after it ends, so the region is bracketed."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, interval_s=0.0005):
         self.index = index
-        self.samples = []
+        self.interval = interval_s
+        self.samples = []          # (sm_mhz, max_mhz, set of reasons)
         self.proc = None
+        self.nvml = None
+        self._run = False
+
+    def _nvml_sample(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+        mask = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        bits = {"hw_slowdown": getattr(n, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(n, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        self.samples.append((float(sm), float(self.max_sm),
+                             {k for k, b in bits.items() if mask & b}))
+
+    def _nvml_loop(self):
+        while self._run:
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
+            time.sleep(self.interval)
 
     def __enter__(self):
-        """Start sampling and block until the first sample arrived (so the whole
-        timed region that follows is bracketed by samples)."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self._nvml_sample()
+            self._run = True
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -97,21 +137,27 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def stop(self):
-        """Wait for one more sample after the timed region, then stop."""
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6 and parts[0].replace(".", "").isdigit():
+                reasons = {self.NAMES[i] for i in range(4) if parts[2 + i].lower() == "active"}
+                mx = float(parts[1]) if parts[1].replace(".", "").isdigit() else 0.0
+                self.samples.append((float(parts[0]), mx, reasons))
+
+    def __exit__(self, *exc):
+        if self.nvml is not None:
+            self._run = False
+            self.thread.join(timeout=2)
+            try:
+                self._nvml_sample()           # one sample after the region
+            except Exception:
+                pass
+            return
         n = len(self.samples)
         t0 = time.time()
         while self.proc is not None and len(self.samples) <= n and time.time() - t0 < 2:
             time.sleep(0.01)
-
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 6:
-                self.samples.append(parts)
-
-    def __exit__(self, *exc):
-        self.stop()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -122,14 +168,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[2] for s in self.samples))),
+                "samples": len(self.samples),
+                "source": "nvml 0.5 ms" if self.nvml is not None else "nvidia-smi 50 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -356,6 +400,7 @@ def run_ours(args):
                        "latent": list(model.spec.latent_resolution) + [16],
                        "mlp": model.spec.decoder_widths(), "head": model.spec.head_kind,
                        "parallelism": f"vertex-shard x{world} + NCCL all-gather",
+                       "sms": sm_count,
                        "l2": "flushed (512 MB write) between timed steps"},
             "roofline": {"bound": "tensor", "kernel": "ndf::tc::query_pp_kernel (+ prep_ws_feat_kernel, prep_ws_merge_kernel)",
                          "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
