@@ -8,7 +8,8 @@ runs in ``libndf_b200.so`` (C-ABI, include/ndf_b200.h).  There is no CPU
 fallback: without the library or a B200 the compute calls raise DeviceError.
 """
 
-from .ensemble import (DeviceEnsemble, EnsembleField, GridDomain, load_ensemble, sample_at,
+from .ensemble import (DeviceEnsemble, EnsembleField, GridDomain, load_ensemble,
+                       load_ensemble_device, sample_at,
                        sample_many, save_ensemble)
 from .errors import (ConfigError, CorruptFileError, DataError, DegenerateSampleError,
                      DeviceError, FormatError, ModelCorruptError, NdfError, NotFoundError,
@@ -30,6 +31,7 @@ __all__ = [
     "ParameterError", "ROLE_MU", "ROLE_NU", "ShapeError", "TrainingError", "UnknownVariableError",
     "benchmark", "difference_field", "digamma", "gaussian_mi_analytic", "grid_positions",
     "ground_truth_field", "ground_truth_field_device", "ksg_mi", "ksg_rows", "load_ensemble",
+    "load_ensemble_device",
     "load_field_grid", "load_model", "matrix_reconstruct", "pair_estimators_device", "pearson",
     "pearson_against", "pearson_rowwise", "reconstruct_field", "reconstruct_field_device",
     "reconstruct_multi_device", "sample_at",

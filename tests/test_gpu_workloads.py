@@ -93,3 +93,38 @@ def test_sharded_query_single_rank_nccl():
         assert torch.equal(got, want)
     finally:
         dist.destroy_process_group()
+
+
+def test_load_ensemble_device_streams_one_variable(tmp_path):
+    """an NDFE variable streamed through pinned double buffers into HBM
+    equals load_ensemble's bytes; truncation / unknown variables / non-finite values
+    raise the reference's errors."""
+    rng = np.random.default_rng(11)
+    vals = rng.standard_normal((3, 37, 5, 9, 13)).astype(np.float32)
+    f = ndf.EnsembleField(ndf.GridDomain(13, 9, 5), ("a", "b", "c"), vals)
+    p = tmp_path / "e.ndfe"
+    ndf.save_ensemble(f, p)
+    host = ndf.load_ensemble(p)
+    for var in ("a", "b", "c"):
+        dev = ndf.load_ensemble_device(p, var, chunk_bytes=1 << 20)   # several chunks
+        assert torch.equal(dev.X.cpu(), torch.from_numpy(np.array(host.member_grids(var))))
+    big = rng.standard_normal((1, 300, 20, 30, 40)).astype(np.float32)   # 28.8 MB > 1 MiB chunks
+    g = ndf.EnsembleField(ndf.GridDomain(40, 30, 20), ("v",), big)
+    q = tmp_path / "big.ndfe"
+    ndf.save_ensemble(g, q)
+    assert torch.equal(ndf.load_ensemble_device(q, "v", chunk_bytes=1 << 20).X.cpu(),
+                       torch.from_numpy(big[0]))
+    with pytest.raises(ndf.UnknownVariableError):
+        ndf.load_ensemble_device(p, "zz")
+    trunc = tmp_path / "t.ndfe"
+    trunc.write_bytes(p.read_bytes()[:-4])
+    with pytest.raises(ndf.CorruptFileError):
+        ndf.load_ensemble_device(trunc, "a")
+    raw = bytearray(p.read_bytes())       # one NaN inside variable "b" (EnsembleField
+    off = len(raw) - vals.nbytes + vals[0].nbytes + 7 * 4   # itself rejects non-finite)
+    raw[off:off + 4] = np.array([np.nan], dtype="<f4").tobytes()
+    r = tmp_path / "nan.ndfe"
+    r.write_bytes(bytes(raw))
+    ndf.load_ensemble_device(r, "a")      # the other variables stay loadable
+    with pytest.raises(ndf.DataError):
+        ndf.load_ensemble_device(r, "b")
