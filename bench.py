@@ -412,7 +412,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 24,
                     "d2h_bytes_per_step": 4 * V,
-                    "api": "paper_2307_02203_b200.reconstruct_field -> FieldGrid (host)"},
+                    "api": "paper_2307_02203_b200.reconstruct_field -> FieldGrid (host)",
+                    "d2h": "kernel stores into pinned host memory (zero-copy)"},
         }
     if not args.quick:
         secondary(args, line, rank, world, dev, peaks, peak_kind, model, w)

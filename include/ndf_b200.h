@@ -108,7 +108,10 @@ int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_bytes, void* st
  * Replaces service.reconstruct_field (service.py:46-84): the ref point is
  * embedded once, every query vertex once; writes out[v - v0] for flat
  * vertices v in [v0, v1).  ref_is_mu selects ROLE_MU / ROLE_NU
- * (service.py:63-80). */
+ * (service.py:63-80).  out may be device memory or page-locked host memory
+ * (cudaHostAlloc / cudaHostRegister): the kernel then stores the field straight
+ * into host RAM over PCIe, no separate D2H copy; pageable memory is rejected
+ * with NDF_ERR_PARAMETER.  Same for ndf_query_points. */
 int ndf_query_grid(const ndf_model_desc* m, double ref_x, double ref_y, double ref_z,
                    int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
                    int64_t v0, int64_t v1, int32_t precision, float* out, void* stream);

@@ -45,6 +45,26 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   return cudaMallocAsync(p, bytes, s);
 }
 
+int resolve_output(void* p, void** dev) {
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("output pointer: ") + cudaGetErrorString(e));
+    return NDF_ERR_PARAMETER;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    *dev = p;
+    return NDF_OK;
+  }
+  if (at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) {
+    *dev = at.devicePointer;   // page-locked host memory: the kernel writes it over PCIe
+    return NDF_OK;
+  }
+  set_error("output must be device memory or page-locked (pinned) host memory");
+  return NDF_ERR_PARAMETER;
+}
+
 }  // namespace ndf
 
 extern "C" int32_t ndf_abi_version(void) { return NDF_ABI_VERSION; }

@@ -50,6 +50,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+// Output buffers may be device memory or page-locked host memory (UVA-mapped):
+// sets *dev to the pointer a kernel stores through; NDF_ERR_PARAMETER for pageable memory.
+int resolve_output(void* p, void** dev);
 
 // ---- exact IEEE fp64 helpers (no FMA contraction) ---------------------------
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }

@@ -331,6 +331,8 @@ extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, dou
   NDF_REQUIRE(v0 >= 0 && v0 <= v1 && v1 <= V, NDF_ERR_PARAMETER, "vertex range out of bounds");
   NDF_REQUIRE(out != nullptr || v0 == v1, NDF_ERR_PARAMETER, "null output");
   if (v0 == v1) return NDF_OK;
+  void* out_dev = nullptr;
+  if ((st = resolve_output(out, &out_dev))) return st;
   QueryArgs a{};
   a.m = *m;
   a.g = make_geom(*m);
@@ -339,7 +341,7 @@ extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, dou
   a.ref[0] = rx; a.ref[1] = ry; a.ref[2] = rz;
   a.nx = nx; a.ny = ny; a.nz = nz;
   a.v0 = v0; a.v1 = v1;
-  a.out = out;
+  a.out = static_cast<float*>(out_dev);
   a.prec = precision;
   if (precision == NDF_PREC_BF16 || precision == NDF_PREC_FP16)
     return launch_query_tc(a, as_stream(stream));
@@ -356,6 +358,8 @@ extern "C" int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int
   NDF_REQUIRE(n_mu == 1 || n_mu == n, NDF_ERR_SHAPE, "p_mu must have 1 or n rows");
   if (n == 0) return NDF_OK;
   NDF_REQUIRE(p_mu && p_nu && out, NDF_ERR_PARAMETER, "null pointer");
+  void* out_dev = nullptr;
+  if ((st = resolve_output(out, &out_dev))) return st;
   QueryArgs a{};
   a.m = *m;
   a.g = make_geom(*m);
@@ -363,7 +367,7 @@ extern "C" int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int
   a.ref_is_mu = 1;
   a.v0 = 0; a.v1 = n;
   a.p_mu = p_mu; a.n_mu = n_mu; a.p_nu = p_nu;
-  a.out = out;
+  a.out = static_cast<float*>(out_dev);
   a.prec = precision;
   if (precision == NDF_PREC_BF16 || precision == NDF_PREC_FP16)
     return launch_query_tc(a, as_stream(stream));

@@ -158,6 +158,29 @@ def test_batch_invariance_and_vertex_ranges(c0):
             assert np.max(np.abs(looped - full[:50])) <= tol
 
 
+def test_pinned_host_output(c0):
+    """reconstruct_field's kernel stores straight into pinned host memory: bitwise the
+    device-resident result; pageable host memory is refused, not faulted on."""
+    w, model = c0
+    ref = w.ref_position()
+    for prec in ("fp32", "bf16", "fp16"):
+        m = model.with_precision(prec)
+        dev = ndf.reconstruct_field_device(m, ref, ndf.ROLE_MU, w.dims).cpu().numpy()
+        host = ndf.reconstruct_field(m, ref, ndf.ROLE_MU, w.dims).values
+        assert np.array_equal(host.reshape(-1), dev)
+        pinned = torch.full((1000,), 7.0, dtype=torch.float32, pin_memory=True)
+        ndf.reconstruct_field_device(m, ref, ndf.ROLE_MU, w.dims, 500, 1500, out=pinned)
+        torch.cuda.synchronize()
+        assert np.array_equal(pinned.numpy(), dev[500:1500])
+    from paper_2307_02203_b200 import _native as N
+    from paper_2307_02203_b200.model import ctypes_ref
+    st = model.device_state()
+    pageable = np.zeros(16, dtype=np.float32)
+    with pytest.raises(ndf.ParameterError):
+        N.call("ndf_query_grid", ctypes_ref(st.desc), 0.0, 0.0, 0.0, 1, 4, 2, 2,
+               0, 16, N.PREC["fp32"], pageable.ctypes.data, N.stream_handle(st.device))
+
+
 def test_constant_decoder_bias():
     """reference tests/test_model.py:99-109."""
     spec = ndf.ModelSpec(grid_resolution=(3, 3, 3), head="linear")
