@@ -479,14 +479,21 @@ struct TcArgs {
 // debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
 constexpr int kTraceTiles = 32, kTraceEvents = 12;
 constexpr int kTraceBase = 6 * kTraceTiles * kTraceEvents;   // + 16 chunk stamps
+// Stamps are compiled only into trace builds (-DNDF_TRACE_BUILD, tools/trace_ws.py):
+// the shipped library carries no clock reads or trace predicates in the hot loops.
+#ifdef NDF_TRACE_BUILD
+#define NDF_TRACE_ON(cond) (t.trace && (cond))
+#else
+#define NDF_TRACE_ON(cond) false
+#endif
 #define NDF_TRACE_AT(slot_, ev)                                                          \
   do {                                                                                   \
-    if (t.trace && blockIdx.x == 0 && wtid == 0 && (slot_) < kTraceTiles)                 \
+    if (NDF_TRACE_ON(blockIdx.x == 0 && wtid == 0 && (slot_) < kTraceTiles))              \
       t.trace[(wg * kTraceTiles + (slot_)) * kTraceEvents + (ev)] = clock64();          \
   } while (0)
 #define NDF_TRACE(ev)                                                                    \
   do {                                                                                   \
-    if (t.trace && blockIdx.x == 0 && wtid == 0 && tcount < kTraceTiles)                  \
+    if (NDF_TRACE_ON(blockIdx.x == 0 && wtid == 0 && tcount < kTraceTiles))               \
       t.trace[(wg * kTraceTiles + tcount) * kTraceEvents + (ev)] = clock64();           \
   } while (0)
 
@@ -676,7 +683,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         for (int c0 = 0; c0 < kHid; c0 += 32) {
           float v[32];
 #define NDF_CHUNK_TRACE(e)                                                                   \
-  if (t.trace && blockIdx.x == 0 && wg == 0 && wtid == 0 && tcount == 3 && l == 1)          \
+  if (NDF_TRACE_ON(blockIdx.x == 0 && wg == 0 && wtid == 0 && tcount == 3 && l == 1))     \
     t.trace[kTraceBase + (c0 >> 5) * 4 + (e)] = clock64();
           NDF_CHUNK_TRACE(0);
           tmem_ld32(tmem_row + (uint32_t)c0, v);          // z (or z/2 for SiLU) incl. bias
@@ -1092,7 +1099,7 @@ query_pp_kernel(const TcArgs t) {
         tmem_wait_ld();
         // debug trace: per-warp stamps of CTA 0, tile 3, layer 1 (tools/trace_ws.py)
 #define NDF_TRACE_WARP(e)                                                                  \
-  if (t.trace && blockIdx.x == 0 && lane == 0 && kk == 3 && l == 1)                      \
+  if (NDF_TRACE_ON(blockIdx.x == 0 && lane == 0 && kk == 3 && l == 1))                 \
     t.trace[kTraceBase + 16 + warp * 8 + (e)] = clock64();
         NDF_TRACE_WARP(0);
         if (l + 1 < H) {

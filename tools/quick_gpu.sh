@@ -4,7 +4,7 @@
 timeout 240 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 180 python bench.py --quick --steps 40 --warmup 5 > gpurun_out/quick.json 2>gpurun_out/quick.err
-timeout 120 python tools/trace_ws.py > gpurun_out/trace_ws.log 2>&1
+[ -f abtest/lib_trace.so ] && NDF_TRACE_LIB=abtest/lib_trace.so timeout 120 python tools/trace_ws.py > gpurun_out/trace_ws.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --quick --steps 2 --warmup 1 > gpurun_out/ncu_launch.log 2>&1
 if [ "${PROFILE:-0}" = 1 ]; then

@@ -3,6 +3,9 @@
 E-WG rows (per tile): acc0 / epi0 / acc1 / epi1 / acc2 / epi2 / out = accumulator ready
 and epilogue done times of the three hidden layers and the output stage.
 P-WG rows (per fill): start, per-vertex words ready, A buffer free, layer-0 MMA issued.
+
+Needs a trace build (stamps are compiled out of the shipped library):
+    bash tools/build_variants.sh trace && NDF_TRACE_LIB=abtest/lib_trace.so python tools/trace_ws.py
 """
 import ctypes
 import os
@@ -18,7 +21,7 @@ from paper_2307_02203_b200 import workloads as W  # noqa: E402
 
 w = W.CONFIGS[1]
 model = W.build_model(w, seed=0, grid_init=1e-4).with_precision("fp16")
-fn = N.load_library().ndf_debug_tc_trace
+fn = N.load_library(os.environ.get("NDF_TRACE_LIB", N.LIB_PATH)).ndf_debug_tc_trace
 fn.argtypes = [ctypes.c_void_p]
 buf = torch.zeros(6 * 32 * 12 + 16 + 16 * 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
