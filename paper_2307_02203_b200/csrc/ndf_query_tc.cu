@@ -770,13 +770,13 @@ __device__ __forceinline__ void issue_ksteps(uint32_t d_tmem, uint32_t a_addr, u
   }
 }
 // A operand in TMEM ("TS" form): K16 steps [k0, k0 + nsteps), step kk's 8 columns at
-// a_col(kk) = a_tmem + 32 (kk / 2) + 8 (kk % 2) (the epilogue packs each 32-column
-// K-chunk's 16-bit activations into the first 16 of its own, already drained, columns).
+// a_col(kk) = a_tmem + 16 kk (the epilogue packs each 16-column sub-chunk's 16-bit
+// activations into the first 8 of its own, already drained, columns).
 __device__ __forceinline__ void issue_ksteps_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_addr,
                                                 int k0, int nsteps, uint32_t sbo_b,
                                                 uint32_t idesc, bool accumulate_first) {
   for (int kk = k0; kk < k0 + nsteps; ++kk) {
-    const uint32_t ac = a_tmem + (uint32_t)(32 * (kk >> 1) + 8 * (kk & 1));
+    const uint32_t ac = a_tmem + (uint32_t)(16 * kk);
     const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
     const uint32_t acc = (kk > k0 || accumulate_first) ? 1u : 0u;
     asm volatile(
@@ -892,10 +892,26 @@ __device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t 
 // its MMA tail the other gets the whole SFU and catches up), so their MMA tails
 // coincide with an idle SFU; half a layer of lag interleaves them (-4.5%).
 #ifndef NDF_ANTIPHASE
-#define NDF_ANTIPHASE 1
+#define NDF_ANTIPHASE (NDF_PP_ISSUER ? 0 : 1)
 #endif
 constexpr int kPPSlots = 2;
-constexpr int kPPThreads = 768;
+// NDF_PP_ISSUER: a dedicated MMA-issuing warp per slot (WG6, warps 24 + s) blocked in
+// bar.sync on the K-chunk barriers, so all 16 epilogue warps drain the same four
+// 16-column sub-chunks per layer (0.302 -> 0.280 ms); register budgets rebalanced with
+// setmaxnreg (launch 72; epilogue 80, producer 72 -- 64 spilled the producer's
+// per-tile state, 0.266 -> 0.259 ms -- issuer 24).
+#ifndef NDF_PP_ISSUER
+#define NDF_PP_ISSUER 1
+#endif
+#ifndef NDF_REG_EPI
+#define NDF_REG_EPI 80
+#endif
+#ifndef NDF_REG_PROD
+#define NDF_REG_PROD 72
+#endif
+#define NDF_STR2(x) #x
+#define NDF_STR(x) NDF_STR2(x)
+constexpr int kPPThreads = NDF_PP_ISSUER ? 896 : 768;
 constexpr int kBiasBlk = 128 * 16 * 2;     // one 128 x 16 16-bit operand block
 
 template <bool F16, bool SILU>
@@ -989,7 +1005,47 @@ query_pp_kernel(const TcArgs t) {
   const uint32_t a_addr = smem_u32(abufs + s * kABytes);
   const uint32_t d_slot = tmem_base + (uint32_t)(s * 2 * kHid);   // + kHid * half
 
+#if NDF_PP_ISSUER
+  if (wg == 6) {
+    // ======================== MMA issuer of slot warp - 24 ===========================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+    const int si = warp - 24;
+    if (si < kPPSlots) {
+      const int64_t fi = (int64_t)blockIdx.x * kPPSlots + si;
+      const int64_t ci = fi < n_tiles ? (n_tiles - fi + tile_stride - 1) / tile_stride : 0;
+      const uint32_t ds = tmem_base + (uint32_t)(si * 2 * kHid);
+      mbar_wait(wbar, 0);
+#pragma unroll 1
+      for (int64_t kk = 0; kk < ci; ++kk) {
+#pragma unroll 1
+        for (int l = 0; l + 1 < H; ++l) {
+          const uint32_t half = (uint32_t)((kk * H + l) & 1);
+          const uint32_t d_next = ds + (half ^ 1u) * kHid;
+          const uint32_t a_tm = ds + half * kHid;                      // A of layer l+1
+          const uint32_t wl = w_addr + lay.w0_bytes + l * lay.wh_bytes;
+#pragma unroll 1
+          for (int k2 = 0; k2 < 4; ++k2) {
+            named_bar(1 + 4 * si + k2, 288);
+            if (lane == 0) {
+              tc_fence_after();
+              if (k2 == 0)
+                mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
+                         smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+              issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+              if (k2 == 3) mma_commit(&acc_full[si]);
+#if NDF_ANTIPHASE
+              if (k2 == NDF_ANTIPHASE && si == 0) atomicAdd(prog0, 1u);
+#endif
+            }
+          }
+        }
+      }
+    }
+  } else if (wg >= 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " NDF_STR(NDF_REG_PROD) ";");
+#else
   if (wg >= 4) {
+#endif
     // ============================ producer (slot s) ==================================
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
@@ -1052,17 +1108,34 @@ query_pp_kernel(const TcArgs t) {
     }
   } else {
     // ======================== epilogue (slot s, column half ch) ======================
+#if NDF_PP_ISSUER
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 " NDF_STR(NDF_REG_EPI) ";");
+#endif
     const int ch = wg & 1;
 #ifndef NDF_ISSUER_Q
 #define NDF_ISSUER_Q 0
 #endif
-    const bool issuer = ch == 0 && wq == NDF_ISSUER_Q;   // warp issuing slot s's MMAs
+    // warp issuing slot s's MMAs (none with a dedicated issuer warp); `lead` arrives
+    // the s_free / d_free mbarriers
+    const bool lead = ch == 0 && wq == NDF_ISSUER_Q;
+#if !NDF_PP_ISSUER
+    const bool issuer = lead;
+#endif
     // K-chunks (32 columns each) drained by this warp.  The issuer's MMA issue blocks
     // it for ~70 cycles per K16 step (tools/micro/mma_issue.cu), so it drains only
     // chunk 0 and its lane-quarter sibling takes chunks 1-3; everyone else drains
     // half a row (chunks 0-1 or 2-3).  MUFU work per sub-partition is unchanged.
+#if NDF_PP_ISSUER
+    // the two column halves interleave by 16-column sub-chunk (ch 0: 0, 2, 4, 6; ch 1: 1,
+    // 3, 5, 7): K-chunk barrier i completes sub-chunks 2i, 2i+1, so chunks complete in
+    // issue order and only one K-chunk (two K16 steps) is left to issue at the end
+    const uint32_t first_col = 16u * (uint32_t)ch;
+#else
     const int kc_begin = wq == NDF_ISSUER_Q ? (ch == 0 ? 0 : 1) : 2 * ch;
     const int kc_end = wq == NDF_ISSUER_Q ? (ch == 0 ? 1 : 4) : 2 * ch + 2;
+    constexpr int kc_step = 1;
+    const uint32_t first_col = 32u * (uint32_t)kc_begin;
+#endif
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     mbar_wait(wbar, 0);
     const float bias_out = vecs[H * kHid];
@@ -1092,10 +1165,10 @@ query_pp_kernel(const TcArgs t) {
         }
 #endif
         tc_fence_after();
-        if (l == 0 && issuer && lane == 0) mbar_arrive(&s_free[s]);   // SMEM A reusable
+        if (l == 0 && lead && lane == 0) mbar_arrive(&s_free[s]);   // SMEM A reusable
         NDF_TRACE_AT((int)kk, 2 * l);
         float va[16], vb[16];
-        tmem_ld16_nowait(d_base + (uint32_t)(32 * kc_begin), va);
+        tmem_ld16_nowait(d_base + first_col, va);
         tmem_wait_ld();
         // debug trace: per-warp stamps of CTA 0, tile 3, layer 1 (tools/trace_ws.py)
 #define NDF_TRACE_WARP(e)                                                                  \
@@ -1109,14 +1182,29 @@ query_pp_kernel(const TcArgs t) {
           const uint32_t d_next = d_slot + (half ^ 1u) * kHid;
           const uint32_t a_tm = d_slot + half * kHid;                  // A of layer l+1
           const uint32_t wl = w_addr + lay.w0_bytes + l * lay.wh_bytes;
+#if NDF_PP_ISSUER
+          (void)d_next; (void)a_tm; (void)wl;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t col = first_col + 32u * (uint32_t)i;
+            float* cur = (i & 1) ? vb : va;
+            float* nxt = (i & 1) ? va : vb;
+            if (i + 1 < 4) tmem_ld16_nowait(d_base + col + 32u, nxt);
+            epilogue16<F16, SILU>(cur, a.m.activation, d_base + col);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            named_bar_arrive(1 + 4 * s + i, 288);     // 8 draining warps + the issuer
+            if (i + 1 < 4) tmem_wait_ld();
+          }
+#else
 #pragma unroll 1
-          for (int kc = kc_begin; kc < kc_end; ++kc) {
+          for (int kc = kc_begin; kc < kc_end; kc += kc_step) {
             const uint32_t col = (uint32_t)(32 * kc);
             tmem_ld16_nowait(d_base + col + 16u, vb);
             epilogue16<F16, SILU>(va, a.m.activation, d_base + col);
             tmem_wait_ld();
-            if (kc + 1 < kc_end) tmem_ld16_nowait(d_base + col + 32u, va);
-            epilogue16<F16, SILU>(vb, a.m.activation, d_base + col + 8u);
+            if (kc + kc_step < kc_end) tmem_ld16_nowait(d_base + col + 32u * kc_step, va);
+            epilogue16<F16, SILU>(vb, a.m.activation, d_base + col + 16u);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             NDF_TRACE_WARP(1 + kc);
             tc_fence_before();
@@ -1143,23 +1231,24 @@ query_pp_kernel(const TcArgs t) {
                 }
               }
             } else {
-              named_bar_arrive(1 + 4 * s + kc, kc == 0 ? 128 : 160);
+              named_bar_arrive(1 + 4 * s + kc, kc == 0 && !NDF_PP_ISSUER ? 128 : 160);
             }
-            if (kc + 1 < kc_end) tmem_wait_ld();
+            if (kc + kc_step < kc_end) tmem_wait_ld();
           }
+#endif
           NDF_TRACE_WARP(6);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
         } else {
           // ---- last hidden layer: A is free for the producer; fp32 output dot ---------
           // layer H-1's MMA has completed, so the other D half (which held layer H-2 and
           // then A of layer H-1) is free for the next tile's layer 0
-          if (issuer && lane == 0) mbar_arrive(&d_free[s]);
+          if (lead && lane == 0) mbar_arrive(&d_free[s]);
           // the output dot product always splits at column 64 (the issuer's lane quarter
           // included), so its fp32 summation order -- and the bits -- never depend on a
           // vertex's row within the tile
           float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          if (kc_begin != 2 * ch) tmem_ld16_nowait(d_base + (uint32_t)(64 * ch), va);
-          if (kc_begin != 2 * ch) tmem_wait_ld();
+          if (first_col != 64u * ch) tmem_ld16_nowait(d_base + 64u * ch, va);
+          if (first_col != 64u * ch) tmem_wait_ld();
 #pragma unroll 1
           for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
             const int col = 32 * kc;
