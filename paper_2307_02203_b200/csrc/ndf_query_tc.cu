@@ -491,6 +491,12 @@ constexpr int kTraceBase = 6 * kTraceTiles * kTraceEvents;   // + 16 chunk stamp
     if (NDF_TRACE_ON(blockIdx.x == 0 && wtid == 0 && (slot_) < kTraceTiles))              \
       t.trace[(wg * kTraceTiles + (slot_)) * kTraceEvents + (ev)] = clock64();          \
   } while (0)
+// per-warp stamps of CTA 0, tile 3, layer 1 (tools/trace_ws.py)
+#define NDF_TRACE_WARP(e)                                                                \
+  do {                                                                                   \
+    if (NDF_TRACE_ON(blockIdx.x == 0 && lane == 0 && kk == 3 && l == 1))                 \
+      t.trace[kTraceBase + 16 + warp * 8 + (e)] = clock64();                             \
+  } while (0)
 #define NDF_TRACE(ev)                                                                    \
   do {                                                                                   \
     if (NDF_TRACE_ON(blockIdx.x == 0 && wtid == 0 && tcount < kTraceTiles))               \
@@ -808,15 +814,51 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
 #define NDF_EXP_TANH(x) tanh_fast(x)
 #endif
 
+// NDF_BIAS_EPI: add the layer's bias in the epilogue (16 broadcast fp32 from SMEM per
+// sub-chunk) instead of the extra ones x bias K16 MMA step per layer.
+#ifndef NDF_BIAS_EPI
+#define NDF_BIAS_EPI 0
+#endif
+__device__ __forceinline__ void add_bias16(float* x, uint32_t bias_saddr) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float b0, b1, b2, b3;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(bias_saddr + 16u * q));
+    x[4 * q] += b0; x[4 * q + 1] += b1; x[4 * q + 2] += b2; x[4 * q + 3] += b3;
+  }
+}
+
 // Hidden-layer epilogue of one 16-column sub-chunk (the bias is already in the
 // accumulator): SiLU (one MUFU tanh per element, weights and bias pre-scaled by
 // 1/2), 16-bit pack, and one tcgen05.st of the 8 packed
 // words into TMEM, where the next layer's MMA reads its A operand (row = lane,
 // K-pairs along the columns).
+#ifndef NDF_EPI_H2
+#define NDF_EPI_H2 0
+#endif
+#ifndef NDF_FFMA2
+#define NDF_FFMA2 1
+#endif
 template <bool F16, bool SILU>
 __device__ __forceinline__ void epilogue16(const float* x, int act, uint32_t a_taddr) {
   float h[16];
-  if constexpr (SILU) {
+  if constexpr (F16 && SILU && NDF_EPI_H2) {
+    uint32_t p[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = silu_h2(x[2 * i], x[2 * i + 1]);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                 ::"r"(a_taddr), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]),
+                 "r"(p[6]), "r"(p[7]) : "memory");
+    return;
+  }
+  if constexpr (SILU && NDF_FFMA2) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#pragma unroll
+    for (int i = 0; i < 16; i += 2)
+      ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);
+  } else if constexpr (SILU) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
 #pragma unroll
@@ -851,14 +893,27 @@ __device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t 
   if constexpr (SILU) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#if NDF_FFMA2
+#pragma unroll
+    for (int i = 0; i < 16; i += 2)
+      ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);
+#else
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = fmaf(x[i], h[i], x[i]);
+#endif
   } else {
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
   }
+#if NDF_FFMA2
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+    ffma2(dots[i & 3], dots[(i & 3) + 1], h[i], h[i + 1], w[i], w[i + 1], dots[i & 3],
+          dots[(i & 3) + 1]);
+#else
 #pragma unroll
   for (int i = 0; i < 16; ++i) dots[i & 3] = fmaf(h[i], w[i], dots[i & 3]);
+#endif
 }
 
 // Ping-pong schedule for single-reference grid queries (sum_absdiff merge; the
@@ -908,6 +963,10 @@ constexpr int kPPSlots = 2;
 #endif
 #ifndef NDF_REG_PROD
 #define NDF_REG_PROD 72
+#endif
+// K-chunks (two K16 steps each) whose MMAs the issuer sends as one burst (1, 2 or 4)
+#ifndef NDF_ISSUE_GROUP
+#define NDF_ISSUE_GROUP 1
 #endif
 #define NDF_STR2(x) #x
 #define NDF_STR(x) NDF_STR2(x)
@@ -1026,17 +1085,21 @@ query_pp_kernel(const TcArgs t) {
 #pragma unroll 1
           for (int k2 = 0; k2 < 4; ++k2) {
             named_bar(1 + 4 * si + k2, 288);
-            if (lane == 0) {
+            NDF_TRACE_WARP(2 * k2);
+            if ((k2 + 1) % NDF_ISSUE_GROUP == 0 && lane == 0) {
               tc_fence_after();
-              if (k2 == 0)
+              const int k_first = 2 * (k2 + 1 - NDF_ISSUE_GROUP);
+              if (k_first == 0 && !NDF_BIAS_EPI)
                 mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
                          smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
-              issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+              issue_ksteps_ts(d_next, a_tm, wl, k_first, 2 * NDF_ISSUE_GROUP, kSboA, idesc,
+                              k_first != 0 || !NDF_BIAS_EPI);
               if (k2 == 3) mma_commit(&acc_full[si]);
 #if NDF_ANTIPHASE
               if (k2 == NDF_ANTIPHASE && si == 0) atomicAdd(prog0, 1u);
 #endif
             }
+            NDF_TRACE_WARP(2 * k2 + 1);
           }
         }
       }
@@ -1099,9 +1162,11 @@ query_pp_kernel(const TcArgs t) {
         else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
         tc_fence_after();
         const uint32_t half = (uint32_t)((kk * H) & 1);
-        mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
-                 smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);       // D = b0
-        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc, true);
+        if (!NDF_BIAS_EPI)
+          mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
+                   smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);     // D = b0
+        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc,
+                     !NDF_BIAS_EPI);
         mma_commit(&acc_full[s]);
       }
       NDF_TRACE_AT((int)kk, 3);
@@ -1140,6 +1205,7 @@ query_pp_kernel(const TcArgs t) {
     mbar_wait(wbar, 0);
     const float bias_out = vecs[H * kHid];
     const uint32_t wout_addr = w_addr + lay.wout_off;
+    const uint32_t bias_s = w_addr + lay.vec_off;   // fp32 biases [H][kHid] (SiLU: pre-scaled)
     uint32_t acc_ph = 0u;
 #if NDF_ANTIPHASE
     // slot 1 starts each hidden layer only once slot 0 is half way through its own
@@ -1170,10 +1236,6 @@ query_pp_kernel(const TcArgs t) {
         float va[16], vb[16];
         tmem_ld16_nowait(d_base + first_col, va);
         tmem_wait_ld();
-        // debug trace: per-warp stamps of CTA 0, tile 3, layer 1 (tools/trace_ws.py)
-#define NDF_TRACE_WARP(e)                                                                  \
-  if (NDF_TRACE_ON(blockIdx.x == 0 && lane == 0 && kk == 3 && l == 1))                 \
-    t.trace[kTraceBase + 16 + warp * 8 + (e)] = clock64();
         NDF_TRACE_WARP(0);
         if (l + 1 < H) {
           // ---- hidden layer l -> A of layer l+1: K-chunk kc (32 columns) is packed into
@@ -1190,10 +1252,12 @@ query_pp_kernel(const TcArgs t) {
             float* cur = (i & 1) ? vb : va;
             float* nxt = (i & 1) ? va : vb;
             if (i + 1 < 4) tmem_ld16_nowait(d_base + col + 32u, nxt);
+            if (NDF_BIAS_EPI) add_bias16(cur, bias_s + 4u * (uint32_t)(l * kHid) + 4u * col);
             epilogue16<F16, SILU>(cur, a.m.activation, d_base + col);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             named_bar_arrive(1 + 4 * s + i, 288);     // 8 draining warps + the issuer
+            NDF_TRACE_WARP(1 + i);
             if (i + 1 < 4) tmem_wait_ld();
           }
 #else
@@ -1253,9 +1317,11 @@ query_pp_kernel(const TcArgs t) {
           for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
             const int col = 32 * kc;
             tmem_ld16_nowait(d_base + (uint32_t)(col + 16), vb);
+            if (NDF_BIAS_EPI) add_bias16(va, bias_s + 4u * (uint32_t)(l * kHid + col));
             dot16<SILU>(va, col, a.m.activation, wout_addr, dots);
             tmem_wait_ld();
             if (kc + 1 < 2 * ch + 2) tmem_ld16_nowait(d_base + (uint32_t)(col + 32), va);
+            if (NDF_BIAS_EPI) add_bias16(vb, bias_s + 4u * (uint32_t)(l * kHid + col + 16));
             dot16<SILU>(vb, col + 16, a.m.activation, wout_addr, dots);
             if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
           }
@@ -1708,7 +1774,8 @@ int launch_query_tc(const QueryArgs& a, cudaStream_t s) { return run_tc(a, nullp
 using namespace ndf;
 
 // Debug only (not part of the C-ABI header): subsequent tensor-core queries record
-// CTA 0's per-phase clock64() stamps into buf[6 * 32 * 12 + 16 + 16 * 8] (NULL disables).
+// CTA 0's per-phase clock64() stamps into buf[6 * 32 * 12 + 16 + 32 * 8] (NULL disables;
+// trace builds only, -DNDF_TRACE_BUILD).
 extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 
 extern "C" size_t ndf_tc_blob_bytes(const ndf_model_desc* m) {

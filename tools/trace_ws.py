@@ -23,7 +23,7 @@ w = W.CONFIGS[1]
 model = W.build_model(w, seed=0, grid_init=1e-4).with_precision("fp16")
 fn = N.load_library(os.environ.get("NDF_TRACE_LIB", N.LIB_PATH)).ndf_debug_tc_trace
 fn.argtypes = [ctypes.c_void_p]
-buf = torch.zeros(6 * 32 * 12 + 16 + 16 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(6 * 32 * 12 + 16 + 32 * 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
     ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
 fn(ctypes.c_void_p(buf.data_ptr()))
@@ -74,10 +74,16 @@ if fine:
     print("layer-1 fine (cycles after acc1): ld0 %.0f  sub0 %.0f  st0 %.0f  kc0 %.0f  st1 %.0f  end %.0f" % tuple(f))
 
 # per-warp stamps of tile 3, layer 1 (E-warps 0..15): start, K-chunk 0..3 stored, end
-w = buf.cpu().numpy()[6 * 32 * 12 + 16:].reshape(16, 8).astype(np.int64)
+w = buf.cpu().numpy()[6 * 32 * 12 + 16:].reshape(32, 8).astype(np.int64)
 if w[0, 0]:
     base = w[:, 0].min()
     print("per-warp layer-1 stamps (tile 3), cycles after the first warp starts:")
+    print("  epilogue warps: start, sub-chunk pair 0..3 stored, end")
     for i in range(16):
         print(f"  warp {i:2d} (slot {i // 8}, half {(i // 4) % 2})", " ".join(
             f"{x - base:6d}" if x else "     -" for x in w[i, [0, 1, 2, 3, 4, 6]]))
+    if w[24, 0]:
+        print("  issuer warps: per K-chunk barrier passed / MMAs issued")
+        for i in (24, 25):
+            print(f"  warp {i:2d} (slot {i - 24})        ", " ".join(
+                f"{x - base:6d}" if x else "     -" for x in w[i]))
