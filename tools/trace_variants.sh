@@ -1,8 +1,6 @@
 #!/bin/bash
-# Schedule trace (tools/trace_ws.py) for each prebuilt abtest/lib_<name>.so.
-cp paper_2307_02203_b200/libndf_b200.so abtest/lib_orig.so
+# Schedule trace (tools/trace_ws.py) for each prebuilt trace build abtest/lib_<name>.so
+# (build with -DNDF_TRACE_BUILD, e.g. tools/build_variants.sh trace).
 for v in "$@"; do
-  cp abtest/lib_$v.so paper_2307_02203_b200/libndf_b200.so
-  echo "== $v"; timeout 120 python tools/trace_ws.py 2>&1 | tail -9
+  echo "== $v"; NDF_TRACE_LIB=abtest/lib_$v.so timeout 120 python tools/trace_ws.py 2>&1 | tail -30
 done
-cp abtest/lib_orig.so paper_2307_02203_b200/libndf_b200.so
