@@ -129,17 +129,27 @@ def check(status: int) -> None:
     raise DeviceError(msg)
 
 
+_CHECKED_DEVICES = {}
+
+
 def require_cuda(device=None):
-    """Return a torch CUDA device or raise DeviceError (no CPU fallback)."""
+    """Return a torch CUDA device or raise DeviceError (no CPU fallback).  A device
+    that passed the checks once is cached (this sits on every query's host path)."""
     import torch
     if not torch.cuda.is_available():
         raise DeviceError("no CUDA device available: the NDF B200 kernels need an sm_100a GPU")
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = torch.cuda.current_device() if device is None else device
+    dev = _CHECKED_DEVICES.get(key) if isinstance(key, (int, str)) else None
+    if dev is not None:
+        return dev
+    dev = torch.device(device) if device is not None else torch.device("cuda", key)
     if dev.type != "cuda":
         raise DeviceError(f"device {dev} is not a CUDA device")
     major, _ = torch.cuda.get_device_capability(dev)
     if major < 10:
         raise DeviceError("libndf_b200 is compiled for sm_100a (B200) only")
+    if isinstance(key, (int, str)):
+        _CHECKED_DEVICES[key] = dev
     return dev
 
 

@@ -396,6 +396,7 @@ class DeviceModel:
             raise ConfigError("model is outside the tcgen05 kernel envelope (L=6, C=16, "
                               "hidden width 128, input width <= 128); use precision='fp32'")
         self.desc = d
+        self.desc_ref = ctypes_ref(d)      # reused by every query call
 
 
 # ---------------------------------------------------------------------------

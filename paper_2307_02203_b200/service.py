@@ -59,9 +59,10 @@ def reconstruct_field_device(model: NdfModel, ref, role: str = ROLE_MU, dims=(64
     ref = np.asarray(ref, dtype=np.float64).reshape(3)
     if out is None:
         out = torch.empty(v1 - v0, dtype=torch.float32, device=st.device)
-    N.call("ndf_query_grid", ctypes_ref(st.desc), float(ref[0]), float(ref[1]), float(ref[2]),
+    N.call("ndf_query_grid", st.desc_ref, float(ref[0]), float(ref[1]), float(ref[2]),
            1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], v0, v1,
-           N.PREC[model.spec.precision], N.ptr(out), N.stream_handle(st.device))
+           N.PREC[model.spec.precision], out.data_ptr(),
+           torch.cuda.current_stream(st.device).cuda_stream)
     if clamp:
         if not out.is_cuda:
             torch.cuda.current_stream(st.device).synchronize()
@@ -87,7 +88,7 @@ def _query_to_host(model: NdfModel, ref, role, dims, clamp) -> np.ndarray:
     saved.  One stream sync; the array owns the pinned block."""
     import torch
     V = dims[0] * dims[1] * dims[2]
-    dev = model.device_state().device
+    dev = model.device_state().device            # raises DeviceError without a GPU
     host = torch.empty(V, dtype=torch.float32, pin_memory=True)
     reconstruct_field_device(model, ref, role, dims, out=host)
     torch.cuda.current_stream(dev).synchronize()

@@ -38,3 +38,14 @@ print("pinned alloc 7 MB      %.3f ms" % t(lambda: torch.empty(V, pin_memory=Tru
 print("query + pinned D2H     %.3f ms" % t(lambda: host.copy_(ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, w.dims, out=out), non_blocking=True)))
 print("reconstruct_field      %.3f ms" % t(lambda: ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims)))
 print("np.empty 7MB + memcpy  %.3f ms" % t(lambda: np.copy(host.numpy())))
+print("query into pinned host  %.3f ms" % t(lambda: ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, w.dims, out=host)))
+st = model.device_state()
+from paper_2307_02203_b200 import _native as N  # noqa: E402
+from paper_2307_02203_b200.model import ctypes_ref  # noqa: E402
+desc = ctypes_ref(st.desc)
+stream = N.stream_handle(st.device)
+prec = N.PREC["fp16"]
+lib = N.load_library()
+hp = host.data_ptr()
+print("raw C-ABI into pinned   %.3f ms" % t(lambda: lib.ndf_query_grid(desc, float(ref[0]), float(ref[1]), float(ref[2]), 1, *w.dims, 0, V, prec, hp, stream)))
+print("empty sync              %.3f ms" % t(lambda: None))
