@@ -25,6 +25,9 @@
 namespace ndf {
 
 constexpr int kKsgThreads = 256;
+#ifndef NDF_KSG_PNET
+#define NDF_KSG_PNET 1           // compare-vector insertion network (knn_scan)
+#endif
 
 struct KsgArgs {
   int mode;                   // 0 ref-vs-node-columns, 1 fp64 rows, 2 vertex-major pairs
@@ -226,12 +229,25 @@ __device__ __forceinline__ double knn_scan(const double* __restrict__ sx,
     if (!(dx < top[KP1 - 1])) break;
     const int j = left ? l : r;
     const double d = fmax(dx, fabs(dsub(yi, yx[j])));
+#if NDF_KSG_PNET
+    // sorted insert from the comparison vector p[s] = d < top[s] (monotone in s, as top
+    // is sorted): slot s takes top[s-1] if d belongs below it, d if it belongs exactly
+    // here; plain compares + selects (no fmin NaN canonicalisation), same values as the
+    // fmin form for every non-NaN d, and a NaN d compares false and changes nothing
+    bool pl[KP1];
+#pragma unroll
+    for (int s = 1; s < KP1; ++s) pl[s] = d < top[s];
+#pragma unroll
+    for (int s = KP1 - 1; s > 1; --s) top[s] = pl[s - 1] ? top[s - 1] : (pl[s] ? d : top[s]);
+    top[1] = pl[1] ? d : top[1];
+#else
     if (d < top[KP1 - 1]) {
       // sorted insert; top[0] is the point itself (distance 0 <= d) and never moves
 #pragma unroll
       for (int s = KP1 - 1; s > 1; --s) top[s] = d < top[s - 1] ? top[s - 1] : fmin(d, top[s]);
       top[1] = fmin(d, top[1]);
     }
+#endif
     if (left) { --l; dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY; }
     else { ++r; dr = r < M ? dsub(sx[r], xi) : INFINITY; }
   }
