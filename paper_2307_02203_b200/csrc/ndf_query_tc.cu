@@ -814,55 +814,26 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
 #define NDF_EXP_TANH(x) tanh_fast(x)
 #endif
 
-// NDF_BIAS_EPI: add the layer's bias in the epilogue (16 broadcast fp32 from SMEM per
-// sub-chunk) instead of the extra ones x bias K16 MMA step per layer.
-#ifndef NDF_BIAS_EPI
-#define NDF_BIAS_EPI 0
-#endif
-__device__ __forceinline__ void add_bias16(float* x, uint32_t bias_saddr) {
+// SiLU of 16 pre-halved accumulators: h = y + y tanh(y) (weights and biases of SiLU
+// layers are pre-scaled by 1/2), one MUFU tanh per element and packed fp32 FMAs
+// (fma.rn.f32x2: same rounding as fmaf, half the issue slots).
+__device__ __forceinline__ void silu16(const float* x, float* h) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float b0, b1, b2, b3;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(bias_saddr + 16u * q));
-    x[4 * q] += b0; x[4 * q + 1] += b1; x[4 * q + 2] += b2; x[4 * q + 3] += b3;
-  }
+  for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+    ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);
 }
 
 // Hidden-layer epilogue of one 16-column sub-chunk (the bias is already in the
-// accumulator): SiLU (one MUFU tanh per element, weights and bias pre-scaled by
-// 1/2), 16-bit pack, and one tcgen05.st of the 8 packed
-// words into TMEM, where the next layer's MMA reads its A operand (row = lane,
-// K-pairs along the columns).
-#ifndef NDF_EPI_H2
-#define NDF_EPI_H2 0
-#endif
-#ifndef NDF_FFMA2
-#define NDF_FFMA2 1
-#endif
+// accumulator): activation, 16-bit pack, and one tcgen05.st of the 8 packed words
+// into TMEM, where the next layer's MMA reads its A operand (row = lane, K-pairs
+// along the columns).
 template <bool F16, bool SILU>
 __device__ __forceinline__ void epilogue16(const float* x, int act, uint32_t a_taddr) {
   float h[16];
-  if constexpr (F16 && SILU && NDF_EPI_H2) {
-    uint32_t p[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) p[i] = silu_h2(x[2 * i], x[2 * i + 1]);
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
-                 ::"r"(a_taddr), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]),
-                 "r"(p[6]), "r"(p[7]) : "memory");
-    return;
-  }
-  if constexpr (SILU && NDF_FFMA2) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
-#pragma unroll
-    for (int i = 0; i < 16; i += 2)
-      ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);
-  } else if constexpr (SILU) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) h[i] = fmaf(x[i], h[i], x[i]);
+  if constexpr (SILU) {
+    silu16(x, h);
   } else {
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
@@ -891,29 +862,16 @@ __device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t 
   }
   float h[16];
   if constexpr (SILU) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
-#if NDF_FFMA2
-#pragma unroll
-    for (int i = 0; i < 16; i += 2)
-      ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);
-#else
-#pragma unroll
-    for (int i = 0; i < 16; ++i) h[i] = fmaf(x[i], h[i], x[i]);
-#endif
+    silu16(x, h);
   } else {
 #pragma unroll
     for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
   }
-#if NDF_FFMA2
+  // dots[c] accumulates elements i = c (mod 4) in ascending i, two lanes per FFMA2
 #pragma unroll
   for (int i = 0; i < 16; i += 2)
     ffma2(dots[i & 3], dots[(i & 3) + 1], h[i], h[i + 1], w[i], w[i + 1], dots[i & 3],
           dots[(i & 3) + 1]);
-#else
-#pragma unroll
-  for (int i = 0; i < 16; ++i) dots[i & 3] = fmaf(h[i], w[i], dots[i & 3]);
-#endif
 }
 
 // Ping-pong schedule for single-reference grid queries (sum_absdiff merge; the
@@ -923,54 +881,36 @@ __device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t 
 //   half (l & 1) while the epilogue drains the other half, so the next layer's MMA
 //   runs underneath the current epilogue (issued 32 K-columns at a time) instead of
 //   after it.  Hidden layers take their A operand from TMEM ("TS" MMA): the epilogue
-//   packs the 16-bit activations into the columns it has just drained, so the
-//   activations never touch shared memory.
-//   WG0-3 -- epilogue: WG 2s+c drains columns [64c, 64c+64) of slot s (4 warps = the
-//            4 TMEM lane quarters), so every SM sub-partition runs four epilogue
-//            warps.  Per 16-column sub-chunk: tcgen05.ld (one ahead), bias + SiLU
-//            (MUFU tanh), pack, tcgen05.st; per 32 columns, one thread of WG 2s issues
-//            that K-chunk's two K16 MMA steps of the next layer.  The last hidden
-//            layer feeds an fp32 dot product with the output weights instead
-//            (partials of the two column halves summed through SMEM) and the head.
+//   packs each 16-column sub-chunk's 16-bit activations into the first 8 of its own,
+//   just drained, columns (K16 step k reads column 16k), so activations never touch
+//   shared memory.
+//   WG0-3 -- epilogue: WG 2s+c with the 4 TMEM lane quarters of slot s; column half c
+//            drains sub-chunks c, c+2, c+4, c+6, so K-chunk i (sub-chunks 2i, 2i+1)
+//            completes i-th.  Per sub-chunk: tcgen05.ld (one ahead), SiLU (MUFU tanh +
+//            FFMA2), pack, tcgen05.st, bar.arrive on K-chunk barrier i.  The last
+//            hidden layer feeds an fp32 dot product with the output weights instead
+//            (the two column halves split at column 64, partials summed through SMEM)
+//            and the head.
 //   WG4, WG5 -- producer of slot 0 / 1: per query tile, the latent words (y/x lerp of
 //            the prep kernel's z-interpolated rows, merged with the reference) and
 //            raw-coordinate words in registers; once the previous layer-0 MMA has
 //            consumed the SMEM A buffer, the pre-merged Fourier groups by cp.async
 //            from the per-query x / (y, z) tables and the registers stored; the
 //            layer-0 MMA is issued once the target accumulator half is drained.
+//   WG6 -- warps 24 + s: the MMA issuer of slot s, blocked in bar.sync on the K-chunk
+//            barriers; each passage issues that K-chunk's two K16 steps of the next
+//            layer (the bias step first), tcgen05.commit after the fourth.  Issuing
+//            blocks the issuing thread until the tensor core accepts the MMA, so a
+//            warp of its own keeps that off the epilogue's critical path (as an
+//            epilogue warp it made its lane quarter the straggler of every layer).
+//   setmaxnreg rebalances the register file: launch 72, epilogue 80, producer 72
+//   (64 spilled its per-tile state), issuer 24.
 // Synchronisation: acc_full[s] (tcgen05.commit of each layer's MMAs), s_free[s]
 // (layer 0's SMEM A consumed: the producer may write the next tile's), d_free[s] (the
 // tile's last MMA has completed: the next tile's layer 0 may target the other D half)
-// and named barriers per K-chunk (warps 1.. arrive, the issuing warp syncs).
-// Slot 1 starts each hidden layer once slot 0 has issued K-chunk NDF_ANTIPHASE of the
-// same layer (0 = uncoupled).  Uncoupled, the two slots phase-lock (while one waits on
-// its MMA tail the other gets the whole SFU and catches up), so their MMA tails
-// coincide with an idle SFU; half a layer of lag interleaves them (-4.5%).
-#ifndef NDF_ANTIPHASE
-#define NDF_ANTIPHASE (NDF_PP_ISSUER ? 0 : 1)
-#endif
+// and named barriers 1 + 4s + i per K-chunk (8 epilogue warps arrive, the issuer syncs).
 constexpr int kPPSlots = 2;
-// NDF_PP_ISSUER: a dedicated MMA-issuing warp per slot (WG6, warps 24 + s) blocked in
-// bar.sync on the K-chunk barriers, so all 16 epilogue warps drain the same four
-// 16-column sub-chunks per layer (0.302 -> 0.280 ms); register budgets rebalanced with
-// setmaxnreg (launch 72; epilogue 80, producer 72 -- 64 spilled the producer's
-// per-tile state, 0.266 -> 0.259 ms -- issuer 24).
-#ifndef NDF_PP_ISSUER
-#define NDF_PP_ISSUER 1
-#endif
-#ifndef NDF_REG_EPI
-#define NDF_REG_EPI 80
-#endif
-#ifndef NDF_REG_PROD
-#define NDF_REG_PROD 72
-#endif
-// K-chunks (two K16 steps each) whose MMAs the issuer sends as one burst (1, 2 or 4)
-#ifndef NDF_ISSUE_GROUP
-#define NDF_ISSUE_GROUP 1
-#endif
-#define NDF_STR2(x) #x
-#define NDF_STR(x) NDF_STR2(x)
-constexpr int kPPThreads = NDF_PP_ISSUER ? 896 : 768;
+constexpr int kPPThreads = 896;
 constexpr int kBiasBlk = 128 * 16 * 2;     // one 128 x 16 16-bit operand block
 
 template <bool F16, bool SILU>
@@ -994,7 +934,6 @@ query_pp_kernel(const TcArgs t) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   float* eref_s = reinterpret_cast<float*>(bars + 16);      // reference latent channels
   float* dotx = reinterpret_cast<float*>(bars + 32);        // [kPPSlots][128] partial dots
-  uint32_t* prog0 = reinterpret_cast<uint32_t*>(bars + 200);  // slot 0: hidden layers half done
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -1011,7 +950,6 @@ query_pp_kernel(const TcArgs t) {
       mbar_init(&s_free[s], 1);
       mbar_init(&d_free[s], 1);
     }
-    *prog0 = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1064,7 +1002,6 @@ query_pp_kernel(const TcArgs t) {
   const uint32_t a_addr = smem_u32(abufs + s * kABytes);
   const uint32_t d_slot = tmem_base + (uint32_t)(s * 2 * kHid);   // + kHid * half
 
-#if NDF_PP_ISSUER
   if (wg == 6) {
     // ======================== MMA issuer of slot warp - 24 ===========================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
@@ -1086,18 +1023,13 @@ query_pp_kernel(const TcArgs t) {
           for (int k2 = 0; k2 < 4; ++k2) {
             named_bar(1 + 4 * si + k2, 288);
             NDF_TRACE_WARP(2 * k2);
-            if ((k2 + 1) % NDF_ISSUE_GROUP == 0 && lane == 0) {
+            if (lane == 0) {
               tc_fence_after();
-              const int k_first = 2 * (k2 + 1 - NDF_ISSUE_GROUP);
-              if (k_first == 0 && !NDF_BIAS_EPI)
+              if (k2 == 0)
                 mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
                          smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
-              issue_ksteps_ts(d_next, a_tm, wl, k_first, 2 * NDF_ISSUE_GROUP, kSboA, idesc,
-                              k_first != 0 || !NDF_BIAS_EPI);
+              issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
               if (k2 == 3) mma_commit(&acc_full[si]);
-#if NDF_ANTIPHASE
-              if (k2 == NDF_ANTIPHASE && si == 0) atomicAdd(prog0, 1u);
-#endif
             }
             NDF_TRACE_WARP(2 * k2 + 1);
           }
@@ -1105,10 +1037,7 @@ query_pp_kernel(const TcArgs t) {
       }
     }
   } else if (wg >= 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 " NDF_STR(NDF_REG_PROD) ";");
-#else
-  if (wg >= 4) {
-#endif
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
     // ============================ producer (slot s) ==================================
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
@@ -1162,59 +1091,27 @@ query_pp_kernel(const TcArgs t) {
         else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
         tc_fence_after();
         const uint32_t half = (uint32_t)((kk * H) & 1);
-        if (!NDF_BIAS_EPI)
-          mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
-                   smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);     // D = b0
-        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc,
-                     !NDF_BIAS_EPI);
+        mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
+                 smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);       // D = b0
+        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc, true);
         mma_commit(&acc_full[s]);
       }
       NDF_TRACE_AT((int)kk, 3);
     }
   } else {
     // ======================== epilogue (slot s, column half ch) ======================
-#if NDF_PP_ISSUER
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 " NDF_STR(NDF_REG_EPI) ";");
-#endif
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
     const int ch = wg & 1;
-#ifndef NDF_ISSUER_Q
-#define NDF_ISSUER_Q 0
-#endif
-    // warp issuing slot s's MMAs (none with a dedicated issuer warp); `lead` arrives
-    // the s_free / d_free mbarriers
-    const bool lead = ch == 0 && wq == NDF_ISSUER_Q;
-#if !NDF_PP_ISSUER
-    const bool issuer = lead;
-#endif
-    // K-chunks (32 columns each) drained by this warp.  The issuer's MMA issue blocks
-    // it for ~70 cycles per K16 step (tools/micro/mma_issue.cu), so it drains only
-    // chunk 0 and its lane-quarter sibling takes chunks 1-3; everyone else drains
-    // half a row (chunks 0-1 or 2-3).  MUFU work per sub-partition is unchanged.
-#if NDF_PP_ISSUER
-    // the two column halves interleave by 16-column sub-chunk (ch 0: 0, 2, 4, 6; ch 1: 1,
-    // 3, 5, 7): K-chunk barrier i completes sub-chunks 2i, 2i+1, so chunks complete in
-    // issue order and only one K-chunk (two K16 steps) is left to issue at the end
+    const bool lead = ch == 0 && wq == 0;           // arrives the s_free / d_free mbarriers
+    // column half ch drains sub-chunks ch, ch+2, ch+4, ch+6 (16 columns each): K-chunk
+    // barrier i completes sub-chunks 2i, 2i+1, so chunks complete in issue order and only
+    // one K-chunk (two K16 steps) is left to issue when the epilogue ends
     const uint32_t first_col = 16u * (uint32_t)ch;
-#else
-    const int kc_begin = wq == NDF_ISSUER_Q ? (ch == 0 ? 0 : 1) : 2 * ch;
-    const int kc_end = wq == NDF_ISSUER_Q ? (ch == 0 ? 1 : 4) : 2 * ch + 2;
-    constexpr int kc_step = 1;
-    const uint32_t first_col = 32u * (uint32_t)kc_begin;
-#endif
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     mbar_wait(wbar, 0);
     const float bias_out = vecs[H * kHid];
     const uint32_t wout_addr = w_addr + lay.wout_off;
-    const uint32_t bias_s = w_addr + lay.vec_off;   // fp32 biases [H][kHid] (SiLU: pre-scaled)
     uint32_t acc_ph = 0u;
-#if NDF_ANTIPHASE
-    // slot 1 starts each hidden layer only once slot 0 is half way through its own
-    // (K-chunk 1 issued), so the two slots' MMA tails fall into each other's epilogues
-    uint32_t seq1 = 0u;
-    const int64_t f0 = (int64_t)blockIdx.x * kPPSlots;
-    const uint32_t total0 = f0 < n_tiles
-        ? (uint32_t)(((n_tiles - f0 + tile_stride - 1) / tile_stride) * (H - 1)) : 0u;
-#endif
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
 #pragma unroll 1
@@ -1223,13 +1120,6 @@ query_pp_kernel(const TcArgs t) {
         const uint32_t d_base = d_slot + lane_base + half * kHid;   // this lane quarter
         mbar_wait(&acc_full[s], acc_ph);
         acc_ph ^= 1u;
-#if NDF_ANTIPHASE
-        if (s == 1 && l + 1 < H) {
-          if (seq1 < total0)
-            while (*(volatile uint32_t*)prog0 < seq1 + 1u) __nanosleep(20);
-          ++seq1;
-        }
-#endif
         tc_fence_after();
         if (l == 0 && lead && lane == 0) mbar_arrive(&s_free[s]);   // SMEM A reusable
         NDF_TRACE_AT((int)kk, 2 * l);
@@ -1238,21 +1128,15 @@ query_pp_kernel(const TcArgs t) {
         tmem_wait_ld();
         NDF_TRACE_WARP(0);
         if (l + 1 < H) {
-          // ---- hidden layer l -> A of layer l+1: K-chunk kc (32 columns) is packed into
-          // the first 16 of its own, just drained, TMEM columns; its two K16 MMA steps of
-          // layer l+1 are issued once the 4 warps owning it have stored it --------------
-          const uint32_t d_next = d_slot + (half ^ 1u) * kHid;
-          const uint32_t a_tm = d_slot + half * kHid;                  // A of layer l+1
-          const uint32_t wl = w_addr + lay.w0_bytes + l * lay.wh_bytes;
-#if NDF_PP_ISSUER
-          (void)d_next; (void)a_tm; (void)wl;
+          // ---- hidden layer l -> A of layer l+1: each sub-chunk's activations are packed
+          // into the first 8 of its own, just drained, TMEM columns; the issuer warp sends
+          // K-chunk i's two K16 steps of layer l+1 once barrier i completes ------------
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t col = first_col + 32u * (uint32_t)i;
             float* cur = (i & 1) ? vb : va;
             float* nxt = (i & 1) ? va : vb;
             if (i + 1 < 4) tmem_ld16_nowait(d_base + col + 32u, nxt);
-            if (NDF_BIAS_EPI) add_bias16(cur, bias_s + 4u * (uint32_t)(l * kHid) + 4u * col);
             epilogue16<F16, SILU>(cur, a.m.activation, d_base + col);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -1260,46 +1144,6 @@ query_pp_kernel(const TcArgs t) {
             NDF_TRACE_WARP(1 + i);
             if (i + 1 < 4) tmem_wait_ld();
           }
-#else
-#pragma unroll 1
-          for (int kc = kc_begin; kc < kc_end; kc += kc_step) {
-            const uint32_t col = (uint32_t)(32 * kc);
-            tmem_ld16_nowait(d_base + col + 16u, vb);
-            epilogue16<F16, SILU>(va, a.m.activation, d_base + col);
-            tmem_wait_ld();
-            if (kc + kc_step < kc_end) tmem_ld16_nowait(d_base + col + 32u * kc_step, va);
-            epilogue16<F16, SILU>(vb, a.m.activation, d_base + col + 16u);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            NDF_TRACE_WARP(1 + kc);
-            tc_fence_before();
-            // K-chunk barriers: chunk 0's writers include the issuer (128 threads); the
-            // other chunks' 4 writers arrive and the issuer waits (160)
-            if (issuer) {
-              named_bar(1 + 4 * s, 128);
-              if (lane == 0) {
-                tc_fence_after();
-                mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
-                         smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
-                issue_ksteps_ts(d_next, a_tm, wl, 0, 2, kSboA, idesc, true);
-              }
-#pragma unroll 1
-              for (int k2 = 1; k2 < 4; ++k2) {
-                named_bar(1 + 4 * s + k2, 160);
-                if (lane == 0) {
-                  tc_fence_after();
-                  issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
-                  if (k2 == 3) mma_commit(&acc_full[s]);
-#if NDF_ANTIPHASE
-                  if (k2 == NDF_ANTIPHASE && s == 0) atomicAdd(prog0, 1u);
-#endif
-                }
-              }
-            } else {
-              named_bar_arrive(1 + 4 * s + kc, kc == 0 && !NDF_PP_ISSUER ? 128 : 160);
-            }
-            if (kc + kc_step < kc_end) tmem_wait_ld();
-          }
-#endif
           NDF_TRACE_WARP(6);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
         } else {
@@ -1307,9 +1151,8 @@ query_pp_kernel(const TcArgs t) {
           // layer H-1's MMA has completed, so the other D half (which held layer H-2 and
           // then A of layer H-1) is free for the next tile's layer 0
           if (lead && lane == 0) mbar_arrive(&d_free[s]);
-          // the output dot product always splits at column 64 (the issuer's lane quarter
-          // included), so its fp32 summation order -- and the bits -- never depend on a
-          // vertex's row within the tile
+          // the output dot product splits at column 64 for every lane quarter, so its fp32
+          // summation order -- and the bits -- never depend on a vertex's row in the tile
           float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
           if (first_col != 64u * ch) tmem_ld16_nowait(d_base + 64u * ch, va);
           if (first_col != 64u * ch) tmem_wait_ld();
@@ -1317,11 +1160,9 @@ query_pp_kernel(const TcArgs t) {
           for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
             const int col = 32 * kc;
             tmem_ld16_nowait(d_base + (uint32_t)(col + 16), vb);
-            if (NDF_BIAS_EPI) add_bias16(va, bias_s + 4u * (uint32_t)(l * kHid + col));
             dot16<SILU>(va, col, a.m.activation, wout_addr, dots);
             tmem_wait_ld();
             if (kc + 1 < 2 * ch + 2) tmem_ld16_nowait(d_base + (uint32_t)(col + 32), va);
-            if (NDF_BIAS_EPI) add_bias16(vb, bias_s + 4u * (uint32_t)(l * kHid + col + 16));
             dot16<SILU>(vb, col + 16, a.m.activation, wout_addr, dots);
             if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
           }

@@ -133,15 +133,6 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
-// SiLU of two pre-halved inputs in packed fp16: h = y + y tanh(y) with the tanh and
-// the FMA on f16x2 (one MUFU and one HFMA2 per pair); returns the packed halves.
-__device__ __forceinline__ uint32_t silu_h2(float y0, float y1) {
-  uint32_t y, t, h;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(y1), "f"(y0));
-  asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(y));
-  asm("fma.rn.f16x2 %0, %1, %2, %1;" : "=r"(h) : "r"(y), "r"(t));
-  return h;
-}
 template <bool F16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   if constexpr (F16) {
