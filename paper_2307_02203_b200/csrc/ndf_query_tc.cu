@@ -1028,7 +1028,11 @@ query_pp_kernel(const TcArgs t) {
               if (k2 == 0)
                 mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
                          smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+#ifndef NDF_EXP_NOKSTEP     // timing experiment: hidden-layer K16 steps skipped (wrong results)
               issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+#else
+              (void)a_tm; (void)wl;
+#endif
               if (k2 == 3) mma_commit(&acc_full[si]);
             }
             NDF_TRACE_WARP(2 * k2 + 1);
@@ -1049,7 +1053,12 @@ query_pp_kernel(const TcArgs t) {
       uint32_t pv[20];    // words 36..55
       {
         float lat[kC];
+#ifdef NDF_EXP_NOPROD    // timing experiment: no latent gather / Fourier copies (wrong results)
+#pragma unroll
+        for (int c = 0; c < kC; ++c) lat[c] = 0.0f;
+#else
         latent_yx_lerp(t.lz, a, ix, iy, iz, lat);
+#endif
 #pragma unroll
         for (int q = 0; q < kC / 4; ++q) {
           const float4 r4 = reinterpret_cast<const float4*>(eref_s)[q];
@@ -1071,12 +1080,16 @@ query_pp_kernel(const TcArgs t) {
       {
         const uint32_t* xs = t.xtab + (size_t)ix * kXTabWords;
         const uint32_t* ys = t.yztab + (size_t)yzrow * kYZTabWords;
+#ifndef NDF_EXP_NOPROD
 #pragma unroll
         for (int g = 0; g < 3; ++g)
           cp_async16(a_addr + canon_off(wtid, 2 * kWordFx + 8 * g, kSboA), xs + 4 * g);
 #pragma unroll
         for (int g = 0; g < 6; ++g)
           cp_async16(a_addr + canon_off(wtid, 2 * kWordFyz + 8 * g, kSboA), ys + 4 * g);
+#else
+        (void)xs; (void)ys;
+#endif
         cp_async_commit();
       }
 #pragma unroll

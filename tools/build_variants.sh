@@ -14,6 +14,9 @@ for v in "$@"; do
     trace) D="-DNDF_TRACE_BUILD";;          # schedule stamps for tools/trace_ws.py
     nomufu) D="-DNDF_EXP_NOMUFU";;          # tanh replaced by an FMA stand-in (wrong results)
     nohint) D="-DNDF_MBAR_HINT=0";;         # mbarrier waits without the suspend hint
+    noks) D="-DNDF_EXP_NOKSTEP";;           # hidden-layer K16 MMAs skipped (wrong results)
+    noprod) D="-DNDF_EXP_NOPROD";;          # producer: no latent gather / Fourier copies (wrong)
+    skel) D="-DNDF_EXP_NOKSTEP -DNDF_EXP_NOMUFU -DNDF_EXP_NOPROD";;
     *) D="$(echo $v | tr ',' ' ')";;        # e.g. -DNDF_MBAR_HINT=2000
   esac
   $NV $D -c paper_2307_02203_b200/csrc/ndf_query_tc.cu -o abtest/q_$v.o &
