@@ -712,7 +712,8 @@ query_tc_kernel(const TcArgs t, const int nwg) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) h[i] = tanh_fast(v[i]);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) h[i] = fmaf(v[i], h[i], v[i]);
+            for (int i = 0; i < 32; i += 2)              // packed fma.rn.f32x2, same bits
+              ffma2(h[i], h[i + 1], v[i], v[i + 1], h[i], h[i + 1], v[i], v[i + 1]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) h[i] = act_f32(a.m.activation, v[i]);
