@@ -20,7 +20,16 @@ namespace ndf {
 constexpr int kTV = 32;               // vertices per tile
 constexpr int kTVP = kTV + 4;         // padded k-row stride (floats)
 constexpr int kThreadsF32 = 128;
-constexpr int kBufFloats = NDF_MAX_WIDTH * kTVP;
+
+// Rows a tile buffer must hold for this model: the widest of the embedding, the
+// encoder layers, the merged decoder input and the decoder layers.  SMEM is sized from
+// it, so narrow models (the reference default: <= 51 rows) fit 4-6 CTAs per SM.
+__host__ __device__ __forceinline__ int f32_buf_rows(const ndf_model_desc& m, int E) {
+  int r = E;
+  for (int i = 0; i <= m.enc_layers && m.enc_layers > 0; ++i) r = r > m.enc_widths[i] ? r : m.enc_widths[i];
+  for (int i = 0; i < m.n_layers; ++i) r = r > m.widths[i] ? r : m.widths[i];
+  return (r + 3) & ~3;
+}
 
 __device__ __forceinline__ int enc_out_dim(const ndf_model_desc& m, int E) {
   return m.enc_layers > 0 ? m.enc_widths[m.enc_layers] : E;
@@ -131,15 +140,16 @@ __device__ __forceinline__ void merge_store(int mode, int C, int i, int v, float
   }
 }
 
-// SMEM: B0, B1 [NDF_MAX_WIDTH][kTVP] (+ B2 for points mode: the mu branch), then two
-// NDF_MAX_WIDTH vectors for the reference's embedding / encoding.
+// SMEM: B0, B1 [rows][kTVP] (+ B2 for points mode: the mu branch; rows = f32_buf_rows),
+// then two NDF_MAX_WIDTH vectors for the reference's embedding / encoding.
 __global__ void __launch_bounds__(kThreadsF32)
 query_f32_kernel(const QueryArgs a) {
   extern __shared__ __align__(16) float smem[];
+  const int buf_floats = f32_buf_rows(a.m, a.g.E) * kTVP;
   float* B0 = smem;
-  float* B1 = B0 + kBufFloats;
-  float* B2 = B1 + kBufFloats;                 // points mode only
-  float* rv0 = a.mode == 1 ? B2 + kBufFloats : B2;
+  float* B1 = B0 + buf_floats;
+  float* B2 = B1 + buf_floats;                 // points mode only
+  float* rv0 = a.mode == 1 ? B2 + buf_floats : B2;
   float* rv1 = rv0 + NDF_MAX_WIDTH;
 
   const int tid = threadIdx.x;
@@ -249,8 +259,8 @@ query_f32_kernel(const QueryArgs a) {
   }
 }
 
-size_t query_f32_smem_bytes(int mode) {
-  return sizeof(float) * ((mode == 1 ? 3 : 2) * (size_t)kBufFloats + 2 * NDF_MAX_WIDTH);
+size_t query_f32_smem_bytes(int mode, int rows = NDF_MAX_WIDTH) {
+  return sizeof(float) * ((mode == 1 ? 3 : 2) * (size_t)rows * kTVP + 2 * NDF_MAX_WIDTH);
 }
 
 int validate_model(const ndf_model_desc* m) {
@@ -301,15 +311,25 @@ int validate_model(const ndf_model_desc* m) {
 
 int launch_query_f32(const QueryArgs& a, cudaStream_t s) {
   static bool attr_set = false;
-  const size_t smem = query_f32_smem_bytes(a.mode);
+  const size_t smem = query_f32_smem_bytes(a.mode, f32_buf_rows(a.m, a.g.E));
   if (!attr_set) {
     NDF_CUDA_CHECK(cudaFuncSetAttribute(query_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)query_f32_smem_bytes(1)));
     attr_set = true;
   }
+  // resident CTAs per SM for this SMEM size (registers cap it at 6), cached per size
+  static thread_local size_t occ_smem = 0;
+  static thread_local int occ_blocks = 1;
+  if (occ_smem != smem) {
+    int b = 0;
+    NDF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, query_f32_kernel, kThreadsF32,
+                                                                 smem));
+    occ_blocks = std::max(b, 1);
+    occ_smem = smem;
+  }
   const int64_t n = a.v1 - a.v0;
   const int64_t tiles = (n + kTV - 1) / kTV;
-  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sm_count() * 3);
+  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sm_count() * occ_blocks);
   query_f32_kernel<<<(unsigned)std::max<int64_t>(grid, 1), kThreadsF32, smem, s>>>(a);
   NDF_LAUNCH_CHECK();
   return NDF_OK;
