@@ -85,13 +85,18 @@ def _query_to_host(model: NdfModel, ref, role, dims, clamp) -> np.ndarray:
     PCIe as it runs (ndf_query_grid accepts pinned host pointers), so there is no
     separate D2H copy after it -- measured on B200 that copy was 0.135 ms of a
     0.47 ms end-to-end query; splitting the launch to overlap it lost more than it
-    saved.  One stream sync; the array owns the pinned block."""
+    saved.  One stream sync; the array owns the pinned block.  (Arguments are already
+    checked by reconstruct_field; this is the per-call host path, kept lean.)"""
     import torch
+    st = model.device_state()                    # raises DeviceError without a GPU
+    ref = np.asarray(ref, dtype=np.float64).reshape(3)
     V = dims[0] * dims[1] * dims[2]
-    dev = model.device_state().device            # raises DeviceError without a GPU
     host = torch.empty(V, dtype=torch.float32, pin_memory=True)
-    reconstruct_field_device(model, ref, role, dims, out=host)
-    torch.cuda.current_stream(dev).synchronize()
+    stream = torch.cuda.current_stream(st.device)
+    N.call("ndf_query_grid", st.desc_ref, float(ref[0]), float(ref[1]), float(ref[2]),
+           1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], 0, V,
+           N.PREC[model.spec.precision], host.data_ptr(), stream.cuda_stream)
+    stream.synchronize()
     arr = host.numpy()
     if clamp:
         np.clip(arr, -1.0, 1.0, out=arr)

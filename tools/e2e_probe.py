@@ -49,3 +49,16 @@ lib = N.load_library()
 hp = host.data_ptr()
 print("raw C-ABI into pinned   %.3f ms" % t(lambda: lib.ndf_query_grid(desc, float(ref[0]), float(ref[1]), float(ref[2]), 1, *w.dims, 0, V, prec, hp, stream)))
 print("empty sync              %.3f ms" % t(lambda: None))
+n = 300
+for _ in range(20):
+    ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims)
+import time as _t
+t0 = _t.perf_counter()
+for _ in range(n):
+    ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims)
+print("reconstruct_field x%d mean %.4f ms" % (n, (_t.perf_counter() - t0) * 1e3 / n))
+t0 = _t.perf_counter()
+for _ in range(n):
+    lib.ndf_query_grid(desc, float(ref[0]), float(ref[1]), float(ref[2]), 1, *w.dims, 0, V, prec, hp, stream)
+    torch.cuda.current_stream().synchronize()
+print("raw C-ABI x%d mean %.4f ms" % (n, (_t.perf_counter() - t0) * 1e3 / n))
