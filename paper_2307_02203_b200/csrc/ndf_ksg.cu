@@ -303,56 +303,54 @@ __global__ void ksg_prep_ref_kernel(const double* __restrict__ ref, const double
 }
 
 #ifndef NDF_KSG_MINBLOCKS
-#define NDF_KSG_MINBLOCKS 3      // 3 CTAs (24 warps) per SM: 1.01 -> 1.17 M pairs/s
+#define NDF_KSG_MINBLOCKS 4      // 4 CTAs (32 warps) per SM at M = 1000 (64 registers)
 #endif
 template <int KP1>
 __global__ void __launch_bounds__(kKsgThreads, NDF_KSG_MINBLOCKS)
 ksg_kernel(const KsgArgs g) {
   extern __shared__ __align__(16) double sm[];
   const int M = g.M, P = g.P;
+  // 48 P + 8 M bytes (56 KB at M = 1000): 4 CTAs (32 warps) per SM
   double* sa = sm;                 // a' sorted ascending (P, +inf padded)
   double* bsa = sa + P;            // b' in a'-order
   double* sb = bsa + P;            // b' sorted ascending (P, +inf padded)
   double* asb = sb + P;            // a' in b'-order
-  double* A0 = asb + P;            // a' in original order (M)
-  double* B0 = A0 + M;             // b' in original order (M)
-  double* terms = B0 + M;          // psi(n_x+1) + psi(n_y+1), original order (M)
-  double* scratch = terms + M;     // 32
-  int* pa = reinterpret_cast<int*>(scratch + 32);   // a'-sorted position -> original index
+  double* terms = asb + P;         // psi(n_x+1) + psi(n_y+1), original order (M)
+  double* scratch = terms;         // block reductions (before terms is written)
+  int* pa = reinterpret_cast<int*>(terms + M);      // a'-sorted position -> original index
   int* pb = pa + P;                                  // b'-sorted position -> original index
-  int* posb = pb + P;                                // original index -> b'-sorted position
+  int* posa = pb + P;                                // original index -> a'-sorted position
+  int* posb = posa + P;                              // original index -> b'-sorted position
   __shared__ int bad_flag;
   const int k = KP1 - 1;
 
   for (int64_t p = blockIdx.x; p < g.n; p += gridDim.x) {
-    // ---- load (fp32 node values are exact in fp64) -----------------------------
-    if (g.mode == 0) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    // ---- load, original order (fp32 node values are exact in fp64) -------------------
+    // mode 0: a' is the reference, already jittered and sorted (ksg_prep_ref_kernel)
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      if (g.mode == 0) {
         sa[i] = g.sa_ref[i];
         pa[i] = g.perm_ref[i];
       }
-    }
-    for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      double a = 0.0, b;
-      if (g.mode == 0) {
-        b = (double)__ldg(g.X + (int64_t)i * g.V + (g.v0 + p));
-      } else if (g.mode == 1) {
-        a = g.A[p * g.a_stride + i];
-        b = g.B[p * (int64_t)M + i];
-      } else {
-        a = (double)__ldg(g.X + g.pa[p] * (int64_t)M + i);
-        b = (double)__ldg(g.X + g.pb[p] * (int64_t)M + i);
+      if (i < M) {
+        if (g.mode == 0) {
+          sb[i] = (double)__ldg(g.X + (int64_t)i * g.V + (g.v0 + p));
+        } else if (g.mode == 1) {
+          sa[i] = g.A[p * g.a_stride + i];
+          sb[i] = g.B[p * (int64_t)M + i];
+        } else {
+          sa[i] = (double)__ldg(g.X + g.pa[p] * (int64_t)M + i);
+          sb[i] = (double)__ldg(g.X + g.pb[p] * (int64_t)M + i);
+        }
       }
-      A0[i] = a;
-      B0[i] = b;
     }
     if (threadIdx.x == 0) bad_flag = 0;
     __syncthreads();
     // ---- ptp + jitter (measures.py:190-192) -------------------------------------
     double bmin = INFINITY, bmax = -INFINITY, amin = INFINITY, amax = -INFINITY;
     for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      bmin = fmin(bmin, B0[i]); bmax = fmax(bmax, B0[i]);
-      if (g.mode != 0) { amin = fmin(amin, A0[i]); amax = fmax(amax, A0[i]); }
+      bmin = fmin(bmin, sb[i]); bmax = fmax(bmax, sb[i]);
+      if (g.mode != 0) { amin = fmin(amin, sa[i]); amax = fmax(amax, sa[i]); }
     }
     bmin = block_reduce(bmin, false, scratch);
     bmax = block_reduce(bmax, true, scratch);
@@ -365,14 +363,10 @@ ksg_kernel(const KsgArgs g) {
     }
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       if (i < M) {
-        const double y = dadd(B0[i], dmul(g.jit[i], scb));
-        B0[i] = y;
-        sb[i] = y;
+        sb[i] = dadd(sb[i], dmul(g.jit[i], scb));
         pb[i] = i;
         if (g.mode != 0) {
-          const double x = dadd(A0[i], dmul(g.jit[i], sca));
-          A0[i] = x;
-          sa[i] = x;
+          sa[i] = dadd(sa[i], dmul(g.jit[i], sca));
           pa[i] = i;
         }
       } else {
@@ -382,14 +376,16 @@ ksg_kernel(const KsgArgs g) {
       }
     }
     __syncthreads();
-    if (g.mode == 0)
-      for (int q = threadIdx.x; q < M; q += blockDim.x) A0[pa[q]] = sa[q];
     if (g.mode != 0) bitonic_sort_kv(sa, pa, P);
     bitonic_sort_kv(sb, pb, P);      // ends with __syncthreads
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      posa[pa[q]] = q;
+      posb[pb[q]] = q;
+    }
+    __syncthreads();
     for (int q = threadIdx.x; q < P; q += blockDim.x) {
-      bsa[q] = q < M ? B0[pa[q]] : 0.0;
-      asb[q] = q < M ? A0[pb[q]] : 0.0;
-      if (q < M) posb[pb[q]] = q;
+      bsa[q] = q < M ? sb[posb[pa[q]]] : 0.0;
+      asb[q] = q < M ? sa[posa[pb[q]]] : 0.0;
     }
     __syncthreads();
     // ---- k-NN (exact, scanned along the sparser axis) + marginal counts ------------
@@ -427,7 +423,7 @@ ksg_kernel(const KsgArgs g) {
 }
 
 size_t ksg_smem_bytes(int M, int P) {
-  return sizeof(double) * (4 * (size_t)P + 3 * (size_t)M + 32) + sizeof(int) * 3 * (size_t)P;
+  return sizeof(double) * (4 * (size_t)P + (size_t)std::max(M, 32)) + sizeof(int) * 4 * (size_t)P;
 }
 
 template <int KP1>
