@@ -49,6 +49,22 @@ void count_launch(int n = 1);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// Per-device record of the dynamic-SMEM size a kernel's attribute has been raised to
+// (cudaFuncSetAttribute is per device); thread-safe, devices 0..63.
+struct SmemAttrCache {
+  size_t bytes[64] = {};
+  template <class K>
+  cudaError_t ensure(K kernel, size_t smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (__atomic_load_n(&bytes[dev], __ATOMIC_ACQUIRE) >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) __atomic_store_n(&bytes[dev], smem, __ATOMIC_RELEASE);
+    return e;
+  }
+};
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 // Output buffers may be device memory or page-locked host memory (UVA-mapped):
 // sets *dev to the pointer a kernel stores through; NDF_ERR_PARAMETER for pageable memory.

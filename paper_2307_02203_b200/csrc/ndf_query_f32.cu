@@ -310,13 +310,9 @@ int validate_model(const ndf_model_desc* m) {
 }
 
 int launch_query_f32(const QueryArgs& a, cudaStream_t s) {
-  static bool attr_set = false;
+  static SmemAttrCache attr;
   const size_t smem = query_f32_smem_bytes(a.mode, f32_buf_rows(a.m, a.g.E));
-  if (!attr_set) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(query_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)query_f32_smem_bytes(1)));
-    attr_set = true;
-  }
+  NDF_CUDA_CHECK(attr.ensure(query_f32_kernel, query_f32_smem_bytes(1)));
   // resident CTAs per SM for this SMEM size (registers cap it at 6), cached per size
   static thread_local size_t occ_smem = 0;
   static thread_local int occ_blocks = 1;

@@ -1481,15 +1481,10 @@ static bool use_ws(const QueryArgs& a, int n_ref, int nwg) {
 template <bool F16, bool SILU, int KIND>
 static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, bool ws,
                        cudaStream_t s) {
-  static size_t attr = 0;
-  if (attr < smem) {
-    NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_tc_kernel<F16, SILU, KIND>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if constexpr (KIND == tc::kGridSingle)
-      NDF_CUDA_CHECK(cudaFuncSetAttribute(tc::query_pp_kernel<F16, SILU>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  static SmemAttrCache attr_tc, attr_pp;
+  NDF_CUDA_CHECK(attr_tc.ensure(tc::query_tc_kernel<F16, SILU, KIND>, smem));
+  if constexpr (KIND == tc::kGridSingle)
+    NDF_CUDA_CHECK(attr_pp.ensure(tc::query_pp_kernel<F16, SILU>, smem));
   if constexpr (KIND != tc::kGridSingle) {
     tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
   } else if (!ws) {
