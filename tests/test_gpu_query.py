@@ -241,6 +241,25 @@ def test_large_grid_bf16_vs_fp32():
     assert np.max(np.abs(a.cpu().numpy()[idx] - want)) <= TOL32
 
 
+def test_vertex_indices_beyond_2_31(c0):
+    """Maximum sizes: a 2048 x 1024 x 1100 output grid (2.3e9 vertices, flat indices past
+    2^31) queried over its last 3,000 vertices and a ragged window across 2^31 --
+    fp32 and 16-bit paths against the oracle at the same flat indices."""
+    _, model = c0
+    dims = (2048, 1024, 1100)
+    V = dims[0] * dims[1] * dims[2]
+    ref = (0.21, -0.4, 0.7)
+    om = oracle_model(model)
+    for v0, v1 in ((V - 3000, V), ((1 << 31) - 777, (1 << 31) + 1234)):
+        want = O.reconstruct_field(om, ref, dims, vertices=np.arange(v0, v1))
+        got32 = ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, dims, v0, v1).cpu().numpy()
+        assert np.max(np.abs(got32 - want)) <= TOL32
+        for prec, tol in (("fp16", TOL16), ("bf16", TOL_BF16)):
+            got = ndf.reconstruct_field_device(model.with_precision(prec), ref, ndf.ROLE_MU, dims,
+                                               v0, v1).cpu().numpy()
+            assert np.max(np.abs(got - want)) <= tol
+
+
 @pytest.mark.parametrize("case", ["mul", "cat", "add2"])
 def test_reference_default_family_golden(golden, case):
     """The reference's own architecture (multi-level HashGrid with dense and hashed
