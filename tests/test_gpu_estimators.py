@@ -258,3 +258,30 @@ def test_pairs_pearson_and_ksg_vs_oracle():
         _, nx, ny = O.ksg_counts_bruteforce(a, b, 8)
         assert np.array_equal(cnt[p, 0], nx) and np.array_equal(cnt[p, 1], ny)
         assert mi[p] == O.ksg_mi(a, b, 8)
+
+
+def test_empty_inputs_everywhere():
+    """Empty ranges and batches return empty results (no launch, no error) on every
+    GPU entry point: query vertex ranges, paired forward, row-wise Pearson, KSG rows,
+    ground-truth vertex ranges, bulk pairs."""
+    import torch
+    spec = ndf.ModelSpec(grid_resolution=(3, 3, 3))
+    model = ndf.NdfModel.build(spec, seed=2)
+    for prec in ("fp32", "fp16"):
+        m = model.with_precision(prec) if prec != "fp32" else model
+        out = ndf.reconstruct_field_device(m, (0, 0, 0), ndf.ROLE_MU, (4, 4, 4), 7, 7)
+        assert out.numel() == 0
+        assert m.forward(np.zeros((0, 3)), np.zeros((0, 3))).shape == (0,)
+    assert ndf.pearson_rowwise(np.zeros((0, 5)), np.zeros((0, 5))).shape == (0,)
+    mi, cnt = ndf.ksg_rows(np.zeros((0, 20)), np.zeros((0, 20)), 3, return_counts=True)
+    assert mi.shape == (0,) and cnt.shape == (0, 2, 20)
+    rng = np.random.default_rng(0)
+    f = field_from(rng.standard_normal((30, 3, 4, 5)).astype(np.float32))
+    for kind in ("pearson", "ksg_mi"):
+        meas = ndf.CorrelationMeasure(kind, ksg_k=3) if kind == "ksg_mi" else ndf.CorrelationMeasure(kind)
+        g = ndf.ground_truth_field_device(f, meas, "v", "v", (0.0, 0.0, 0.0), (5, 4, 3), 11, 11)
+        assert g.numel() == 0
+    res = ndf.pair_estimators_device(f, "v", np.zeros(0, np.int64), np.zeros(0, np.int64), k=3)
+    for v in (res.values() if isinstance(res, dict) else res):
+        assert len(v) == 0
+    torch.cuda.synchronize()
