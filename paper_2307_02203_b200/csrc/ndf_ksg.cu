@@ -131,23 +131,6 @@ __device__ __forceinline__ int upper_bound_le(const double* s, int P, double x) 
   return lo;
 }
 
-__device__ void bitonic_sort2(double* a, double* b, int P) {
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = ((lo & size) == 0);
-        double x = a[lo], y = a[hi];
-        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
-        x = b[lo]; y = b[hi];
-        if ((x > y) == up) { b[lo] = y; b[hi] = x; }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 __device__ __forceinline__ double block_reduce(double v, bool is_max, double* scratch) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -173,8 +156,8 @@ __device__ __forceinline__ double block_reduce(double v, bool is_max, double* sc
   return v;
 }
 
-// Bitonic sort of P = 2^m keys with an int payload (ascending by key).
-__device__ void bitonic_sort_kv(double* key, int* val, int P) {
+// Bitonic sort of P = 2^m keys with an int payload (ascending by key), all in SMEM.
+__device__ void bitonic_sort_kv_smem(double* key, int* val, int P) {
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
@@ -192,18 +175,73 @@ __device__ void bitonic_sort_kv(double* key, int* val, int P) {
   }
 }
 
-__device__ void bitonic_sort_k(double* key, int P) {
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+// Compare-exchange of this lane's element (global index e, key k, payload v) with its
+// partner at e ^ stride held by lane ^ stride (stride <= 16): keep the smaller key if
+// the element is the lower of the pair in an ascending run, the larger otherwise.
+// Equal keys never move, so the two lanes always keep complementary elements.
+__device__ __forceinline__ void bitonic_lane_step(double& k, int& v, int e, int stride, int size) {
+  const double pk = __shfl_xor_sync(0xffffffffu, k, stride);
+  const int pv = __shfl_xor_sync(0xffffffffu, v, stride);
+  const bool take_min = ((e & stride) == 0) == ((e & size) == 0);
+  if (take_min ? pk < k : pk > k) { k = pk; v = pv; }
+}
+
+// Strides min(size/2, 32) .. 1 of bitonic merge stage(s) `size_lo..size_hi` on 64-element
+// segments held in registers (lane holds elements lane and lane + 32 of its segment):
+// the sub-64 strides need no shared-memory round trip and no block barrier.
+__device__ __forceinline__ void bitonic_segment_phase(double* key, int* val, int P, int size_lo,
+                                                      int size_hi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int seg = warp; seg < P / 64; seg += nw) {
+    const int e0 = seg * 64 + lane, e1 = e0 + 32;
+    double k0 = key[e0], k1 = key[e1];
+    int v0 = val[e0], v1 = val[e1];
+    for (int size = size_lo; size <= size_hi; size <<= 1) {
+      for (int stride = min(size >> 1, 32); stride > 0; stride >>= 1) {
+        if (stride == 32) {
+          // pair (e0, e1) within the lane; e0 is the lower element
+          if ((k0 > k1) == ((e0 & size) == 0)) {
+            const double tk = k0; k0 = k1; k1 = tk;
+            const int tv = v0; v0 = v1; v1 = tv;
+          }
+        } else {
+          bitonic_lane_step(k0, v0, e0, stride, size);
+          bitonic_lane_step(k1, v1, e1, stride, size);
+        }
+      }
+    }
+    key[e0] = k0; key[e1] = k1;
+    val[e0] = v0; val[e1] = v1;
+  }
+}
+
+// Same sort with every stride below 64 done in registers (warp shuffles): for P = 1024,
+// 10 shared-memory compare-exchange stages and 15 block barriers instead of 55 of each.
+// The sorted keys are the same; only the order of equal keys may differ, which no
+// consumer observes (ranks, distances and counts depend on values alone).
+__device__ void bitonic_sort_kv(double* key, int* val, int P) {
+  if (P < 64) {
+    bitonic_sort_kv_smem(key, val, P);
+    return;
+  }
+  bitonic_segment_phase(key, val, P, 2, 64);       // sizes 2..64 entirely in registers
+  __syncthreads();
+  for (int size = 128; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride >= 64; stride >>= 1) {
       for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
         const int lo = 2 * t - (t & (stride - 1));
         const int hi = lo + stride;
         const bool up = ((lo & size) == 0);
         const double x = key[lo], y = key[hi];
-        if ((x > y) == up) { key[lo] = y; key[hi] = x; }
+        if ((x > y) == up) {
+          key[lo] = y; key[hi] = x;
+          const int v = val[lo]; val[lo] = val[hi]; val[hi] = v;
+        }
       }
       __syncthreads();
     }
+    bitonic_segment_phase(key, val, P, size, size);
+    __syncthreads();
   }
 }
 
