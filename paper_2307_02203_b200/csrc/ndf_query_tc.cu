@@ -3,32 +3,35 @@
 //   embed (fp64 -> fp32, bit-exact with model.py:169-177)
 //   -> merge [e_r + e_q, |e_r - e_q|]                      (model.py:279-286 + BASELINE)
 //   -> H x { tcgen05.mma 16-bit x 16-bit -> fp32 accumulator in TMEM ;
-//            tcgen05.ld epilogue: bias + activation, packed back to SMEM as the
-//            next layer's A operand }
-//   -> output layer 128 -> 1 as a 16-column tcgen05.mma (zero-padded B) -> head.
+//            tcgen05.ld epilogue: activation, packed back as the next layer's A }
+//   -> output layer 128 -> 1 -> head.
 //
-// Layout / schedule (one persistent CTA per SM, NWG <= 4 warpgroups):
-//   * the packed parameter blob (UMMA-canonical K-major 16-bit weights + fp32 bias
-//     vectors) is fetched once per CTA by the bulk-copy engine (cp.async.bulk ->
-//     mbarrier complete_tx) and stays resident in SMEM;
-//   * each warpgroup owns a 128-row tile of query vertices, one 32 KB A buffer
-//     (SWIZZLE_NONE canonical layout: 8x16 B core matrices, LBO = 128 B along K,
-//     SBO = 2048 B along M) and 128 TMEM columns holding the fp32 accumulator
-//     (row m of the tile = TMEM lane m = thread m of the warpgroup);
-//   * one thread per warpgroup issues the K/16 tcgen05.mma steps of a layer and
-//     commits them to the warpgroup's mbarrier; while one warpgroup runs its
-//     epilogue, the other warpgroups' MMAs keep the tensor pipe busy -- a 4-way
-//     ping-pong without any CTA-wide barrier.
-//   * every accumulator is pre-loaded with its layer's bias (tcgen05.st while the
-//     previous layer's values are drained), so the MMAs accumulate onto the bias
-//     and the epilogue has no bias adds;
-//   * SiLU layers are packed with W and b pre-scaled by 1/2 (exact in 16-bit), so
-//     the accumulator holds x/2 and silu(x) = x/2 + (x/2)*tanh(x/2) is one
-//     tanh.approx (MUFU) and one FMA per element, then a paired 16-bit pack.
-//   * grid-mode Fourier features are per-axis: a prep kernel evaluates them once
-//     per axis node (same fp64 sincos, so the same bits) and the query reads them.
-//   * multi-reference queries (BASELINE config 3) embed each query vertex once and
-//     reuse it for every reference (refs' embeddings come from the prep kernel).
+// Two schedules share the packed parameter blob (UMMA-canonical K-major 16-bit
+// weights + fp32 bias vectors, fetched once per CTA by the bulk-copy engine and kept
+// resident in SMEM) and the SiLU trick (W and b of SiLU layers pre-scaled by 1/2,
+// exact in 16-bit, so silu(x) = y + y tanh(y) with y = x/2: one MUFU tanh and one
+// FMA per element):
+//
+// * query_pp_kernel (default for single-reference grid queries, the BASELINE hot
+//   path): per CTA two "slots" of 128 query vertices, each with two TMEM accumulator
+//   halves so layer l+1's MMAs run underneath layer l's epilogue, hidden-layer A
+//   operands taken straight from TMEM, dedicated producer and MMA-issuer warps, and
+//   the output layer as an fp32 dot product.  See the comment above the kernel.
+//
+// * query_tc_kernel ("classic"; multi-reference cubes, paired/points forward, the
+//   reference's other merges): one CTA per SM with up to 4 symmetric warpgroups,
+//   each owning a 128-row tile, one 32 KB SMEM A buffer (SWIZZLE_NONE canonical:
+//   8x16 B core matrices, LBO = 128 B along K, SBO = 2048 B along M) and 128 TMEM
+//   columns (row m of the tile = TMEM lane m = thread m of the warpgroup); one thread
+//   per warpgroup issues a layer's K/16 MMAs and commits them to the warpgroup's
+//   mbarrier, so while one warpgroup runs its epilogue the others keep the tensor
+//   pipe busy.  Accumulators are pre-loaded with the next layer's bias (tcgen05.st)
+//   and the output layer is a 16-column tcgen05.mma (zero-padded B).  Multi-reference
+//   queries (BASELINE config 3) embed each query vertex once and reuse it for every
+//   reference.
+//
+// Grid-mode Fourier features are per-axis: prep kernels evaluate them once per axis
+// node (the same fp64 sincos, so the same bits) and the queries read them.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
