@@ -26,6 +26,9 @@ Fixtures (all inputs seeded, outputs produced by the reference itself):
                      (parameter checksums and outputs).
 * ``pearson.npz``    pearson / pearson_against / pearson_rowwise and
                      ground_truth_field(pearson) (measures.py:59-133, 273-295).
+* ``activations.npz`` nn.activation (nn.py:23-32) -- relu, snake, snake_alt --
+                     on seeded float32 inputs spanning [-40, 40]
+                     (``python make_golden.py activations`` rewrites only this one).
 * ``ksg.npz``        ksg_mi (measures.py:173-203) on seeded vectors incl.
                      duplicates and a constant vector, plus
                      ground_truth_field(ksg_mi) (measures.py:296-314), plus the
@@ -221,5 +224,24 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+def activations():
+    sys.path.insert(0, REF_SRC)
+    import ndf
+    from ndf.nn import activation
+    assert ndf.__file__.startswith(REF_SRC), ndf.__file__
+    rng = np.random.default_rng(11)
+    x = np.concatenate([rng.standard_normal(4096) * 3.0, rng.uniform(-40, 40, 4096),
+                        [0.0, -0.0, 1e-30, -1e-30, 40.0, -40.0]]).astype(np.float32)
+    arrays = {"x": x}
+    for kind in ("relu", "snake", "snake_alt"):
+        arrays[kind] = activation(kind, x)
+    np.savez_compressed(os.path.join(HERE, "activations.npz"), **arrays)
+    print("activations.npz written to", HERE)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["activations"]:
+        activations()
+    else:
+        main()
+        activations()

@@ -165,3 +165,12 @@ def test_reference_default_restatement_bitwise(golden):
     dims = tuple(int(x) for x in g["dims"])
     assert np.array_equal(O.reconstruct_field(om, g["refs"][0], dims), g["default_out0"])
     assert np.array_equal(om.forward(g["p1"], g["p2"]), g["default_fwd"])
+
+
+def test_activations_golden_bitwise(golden):
+    """nn.py:23-32 (relu, snake, snake_alt) reproduced bit for bit on [-40, 40]."""
+    g = golden("activations")
+    for kind in ("relu", "snake", "snake_alt"):
+        got = O.activation(kind, g["x"])
+        assert got.dtype == np.float32
+        assert np.array_equal(got, g[kind]), kind

@@ -20,6 +20,7 @@ def rnd(x, dt):
 
 
 w = W.CONFIGS[0]
+act = sys.argv[1] if len(sys.argv) > 1 else "silu"     # hidden activation to simulate
 for gi in (1.0, 1e-4):
     m = W.build_model(w, seed=0, grid_init=gi)
     ref = w.ref_position()
@@ -27,7 +28,7 @@ for gi in (1.0, 1e-4):
     a = O.embed(np.asarray(ref).reshape(1, 3), m.grid_mu, 6)
     q = O.embed(pos, m.grid_nu, 6)
     x = O.merge("sum_absdiff", np.broadcast_to(a, q.shape), q)
-    exact = O.head("tanh", O.mlp_forward(m.weights, m.biases, "silu", x))[:, 0]
+    exact = O.head("tanh", O.mlp_forward(m.weights, m.biases, act, x))[:, 0]
 
     def sim(round_w, round_a, dt):
         h = rnd(x, dt) if round_a else x
@@ -37,7 +38,7 @@ for gi in (1.0, 1e-4):
             z = (h.astype(np.float64) @ ww.astype(np.float64) + b).astype(np.float32)
             if i == L - 1:
                 return np.tanh(z)[:, 0]
-            h = O.activation("silu", z)
+            h = O.activation(act, z)
             if round_a and i < L - 2:
                 h = rnd(h, dt)
 
