@@ -132,6 +132,28 @@ def test_c0_other_activations_16bit(c0, act):
         assert np.max(np.abs(m.forward(p1, p2) - want_pts)) <= tol, (act, prec)
 
 
+def test_c0_concat_merge_16bit(c0):
+    """concat (model.py:279-286) shares sum_absdiff's interleaved two-block A layout
+    but runs on the classic schedule: grid query and paired forward vs the oracle."""
+    w, base = c0
+    from dataclasses import replace
+    model = ndf.NdfModel(replace(base.spec, merge="concat", head="tanh"), base.grid_mu,
+                         base.grid_nu, base.weights, base.biases)
+    ref = w.ref_position()
+    om = oracle_model(model)
+    want = O.reconstruct_field(om, ref, w.dims)
+    rng = np.random.default_rng(12)
+    p1, p2 = rng.uniform(-1, 1, (400, 3)), rng.uniform(-1, 1, (400, 3))
+    want_pts = om.forward(p1, p2)
+    assert np.max(np.abs(ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims).values - want)) <= TOL32
+    for prec, tol in (("fp16", TOL16), ("bf16", TOL_BF16)):
+        m = model.with_precision(prec)
+        assert np.max(np.abs(ndf.reconstruct_field(m, ref, ndf.ROLE_MU, w.dims).values - want)) <= tol
+        assert np.max(np.abs(ndf.reconstruct_field(m, ref, ndf.ROLE_NU, w.dims).values -
+                             O.reconstruct_field(om, ref, w.dims, role="reference-is-nu"))) <= tol
+        assert np.max(np.abs(m.forward(p1, p2) - want_pts)) <= tol
+
+
 def test_c0_off_node_ref_and_other_dims(c0):
     w, model = c0
     for ref, dims in [((0.123, -0.77, 0.5), w.dims), ((1.3, -2.0, 0.0), (17, 9, 5)),
