@@ -285,3 +285,24 @@ def test_empty_inputs_everywhere():
     for v in (res.values() if isinstance(res, dict) else res):
         assert len(v) == 0
     torch.cuda.synchronize()
+
+
+def test_ksg_extreme_sizes():
+    """Size envelope of the GPU KSG: the smallest sample (M=2, k=1), the largest
+    (M=4096 -- 224 KB of SMEM per pair, one CTA per SM -- with k=16), bit-exact counts
+    and MI vs the oracle; past the envelope a ConfigError, not a fault."""
+    rng = np.random.default_rng(21)
+    for M, k, B in ((2, 1, 3), (3, 2, 3), (4096, 16, 3), (4096, 1, 2)):
+        a = rng.standard_normal(M).astype(np.float32).astype(np.float64)
+        b = np.stack([(0.6 * a + rng.standard_normal(M)).astype(np.float32).astype(np.float64)
+                      for _ in range(B)])
+        mi, counts = ndf.ksg_rows(a, b, k, return_counts=True)
+        for s in range(B):
+            assert mi[s] == O.ksg_mi(a, b[s], k), (M, k)
+            if M <= 64:
+                _, nx, ny = O.ksg_counts_bruteforce(a, b[s], k)
+                assert np.array_equal(counts[s, 0], nx) and np.array_equal(counts[s, 1], ny)
+    with pytest.raises(ndf.ConfigError):
+        ndf.ksg_rows(np.zeros(4097), np.zeros((1, 4097)), 3)
+    with pytest.raises(ndf.ConfigError):
+        ndf.ksg_rows(np.arange(40.0), np.arange(40.0)[None], 17)
