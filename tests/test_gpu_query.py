@@ -154,6 +154,29 @@ def test_c0_concat_merge_16bit(c0):
         assert np.max(np.abs(m.forward(p1, p2) - want_pts)) <= tol
 
 
+@pytest.mark.parametrize("layers", [2, 5, 6])
+def test_decoder_depth_envelope(layers):
+    """Decoder depth on the tensor cores: 1 hidden layer, and 4 / 5 hidden layers (the
+    SMEM-resident weights leave room for only 3 / 2 classic warpgroups) vs the fp32
+    oracle; a decoder too deep for SMEM is refused at upload with ConfigError."""
+    spec = ndf.ModelSpec(grid_resolution=(4, 6, 2), decoder_layers=layers, channels=128,
+                         head="tanh", grid_init=1.0)
+    model = ndf.NdfModel.build(spec, seed=4)
+    rng = np.random.default_rng(8)
+    for b in model.biases:
+        b[:] = rng.uniform(-0.2, 0.2, b.shape).astype(np.float32)
+    om = oracle_model(model)
+    ref, dims = (0.2, -0.3, 0.5), (21, 13, 5)
+    want = O.reconstruct_field(om, ref, dims)
+    for prec, tol in (("fp16", TOL16), ("bf16", TOL_BF16)):
+        got = ndf.reconstruct_field(model.with_precision(prec), ref, ndf.ROLE_MU, dims).values
+        assert np.max(np.abs(got - want)) <= tol, (layers, prec)
+    deep = ndf.NdfModel.build(ndf.ModelSpec(grid_resolution=(4, 6, 2), decoder_layers=9,
+                                            channels=128, precision="fp16"), seed=4)
+    with pytest.raises(ndf.ConfigError):
+        deep.forward(np.zeros((1, 3)), np.zeros((1, 3)))
+
+
 def test_c0_off_node_ref_and_other_dims(c0):
     w, model = c0
     for ref, dims in [((0.123, -0.77, 0.5), w.dims), ((1.3, -2.0, 0.0), (17, 9, 5)),
