@@ -507,6 +507,9 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
     pa_all, pb_all = W.pair_list(W.CONFIGS[4], count=n_pairs, seed=2)
     p0, p1 = min(n_pairs, rank * math.ceil(n_pairs / world)), min(n_pairs, (rank + 1) * math.ceil(n_pairs / world))
     ens2.vertex_major()
+    # warm-up on a slice (kernel attributes, psi / jitter tables, allocator), then time
+    ndf.pair_estimators_device(ens2, "v", pa_all[p0:p0 + 1024], pb_all[p0:p0 + 1024],
+                               k=W.CONFIGS[4].ksg_k)
     torch.cuda.synchronize()
     t0.record(stream)
     res = ndf.pair_estimators_device(ens2, "v", pa_all[p0:p1], pb_all[p0:p1], k=W.CONFIGS[4].ksg_k)
