@@ -1,6 +1,10 @@
 """Per-phase schedule of the tcgen05 query kernel (CTA 0), from clock64 stamps.
 
-    python tools/trace_tc.py [--precision fp16]
+    bash tools/build_variants.sh trace
+    NDF_TC_SCHEDULE=classic NDF_TRACE_LIB=abtest/lib_trace.so python tools/trace_tc.py [--precision fp16]
+
+(stamps are compiled only into trace builds; the classic schedule runs single-reference
+queries only when NDF_TC_SCHEDULE=classic)
 
 Events per tile: 0 start, 1 layer-0 A written, 2/4/6 hidden-layer MMA done,
 3/5/7 epilogue done, 10 output MMA done.
@@ -27,10 +31,10 @@ def main():
     args = ap.parse_args()
     w = W.CONFIGS[1]
     model = W.build_model(w, seed=0, grid_init=1e-4).with_precision(args.precision)
-    lib = N.load_library()
+    lib = N.load_library(os.environ.get("NDF_TRACE_LIB", N.LIB_PATH))
     fn = lib.ndf_debug_tc_trace
     fn.argtypes = [ctypes.c_void_p]
-    buf = torch.zeros(6 * 32 * 12 + 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(6 * 32 * 12 + 16 + 32 * 8, dtype=torch.int64, device="cuda")
     for _ in range(3):
         ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
     fn(ctypes.c_void_p(buf.data_ptr()))
