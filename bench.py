@@ -413,7 +413,9 @@ def run_ours(args):
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 24,
                     "d2h_bytes_per_step": 4 * V,
                     "api": "paper_2307_02203_b200.reconstruct_field -> FieldGrid (host)",
-                    "d2h": "kernel stores into pinned host memory (zero-copy)"},
+                    "d2h": "kernel stores into pinned host memory (zero-copy)",
+                    "scope": "one GPU (rank 0): the public call is single-device"
+                             if world > 1 else "one GPU"},
         }
     if not args.quick:
         secondary(args, line, rank, world, dev, peaks, peak_kind, model, w)
