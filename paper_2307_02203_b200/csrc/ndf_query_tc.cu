@@ -998,7 +998,10 @@ query_pp_kernel(const TcArgs t) {
   const int H = lay.H;
 
   const int64_t n = a.v1 - a.v0;
-  const int64_t n_tiles = (n + kTileM - 1) / kTileM;
+  // multi-reference cubes: tile T covers vertex tile T % n_vt of reference T / n_vt, so
+  // concurrently running tiles share one reference's tables in L2
+  const int64_t n_vt = (n + kTileM - 1) / kTileM;
+  const int64_t n_tiles = n_vt * t.n_ref;
   const int64_t tile_stride = (int64_t)gridDim.x * kPPSlots;
   const int s = wg < 4 ? (wg >> 1) : wg - 4;        // slot of this warpgroup
   const int64_t first = (int64_t)blockIdx.x * kPPSlots + s;
@@ -1049,7 +1052,11 @@ query_pp_kernel(const TcArgs t) {
     // ============================ producer (slot s) ==================================
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
-      const int64_t tile = first + kk * tile_stride;
+      const int64_t tile_g = first + kk * tile_stride;
+      const int r = t.n_ref == 1 ? 0 : (int)((uint32_t)tile_g / (uint32_t)n_vt);
+      const int64_t tile = tile_g - (int64_t)r * n_vt;
+      const uint32_t* xtab = t.xtab + (size_t)r * a.nx * kXTabWords;
+      const uint32_t* yztab = t.yztab + (size_t)r * a.ny * a.nz * kYZTabWords;
       NDF_TRACE_AT((int)kk, 0);
       int ix, iy, iz;
       tile_node(a, tile, wtid, ix, iy, iz);
@@ -1065,15 +1072,17 @@ query_pp_kernel(const TcArgs t) {
 #endif
 #pragma unroll
         for (int q = 0; q < kC / 4; ++q) {
-          const float4 r4 = reinterpret_cast<const float4*>(eref_s)[q];
+          const float4 r4 = t.n_ref == 1
+              ? reinterpret_cast<const float4*>(eref_s)[q]
+              : __ldg(reinterpret_cast<const float4*>(t.erefs + (size_t)r * kERefStride) + q);
           const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             pv[4 * q + u] = pack2<F16>(rv[u] + lat[4 * q + u], fabsf(rv[u] - lat[4 * q + u]));
         }
-        pv[16] = __ldg(t.xtab + (size_t)ix * kXTabWords + 12);
+        pv[16] = __ldg(xtab + (size_t)ix * kXTabWords + 12);
         const uint2 ryz =
-            __ldg(reinterpret_cast<const uint2*>(t.yztab + (size_t)yzrow * kYZTabWords + 24));
+            __ldg(reinterpret_cast<const uint2*>(yztab + (size_t)yzrow * kYZTabWords + 24));
         pv[17] = ryz.x;
         pv[18] = ryz.y;
         pv[19] = 0u;
@@ -1082,8 +1091,8 @@ query_pp_kernel(const TcArgs t) {
       if (kk >= 1) mbar_wait(&s_free[s], (uint32_t)((kk - 1) & 1));   // previous layer 0 done
       NDF_TRACE_AT((int)kk, 2);
       {
-        const uint32_t* xs = t.xtab + (size_t)ix * kXTabWords;
-        const uint32_t* ys = t.yztab + (size_t)yzrow * kYZTabWords;
+        const uint32_t* xs = xtab + (size_t)ix * kXTabWords;
+        const uint32_t* ys = yztab + (size_t)yzrow * kYZTabWords;
 #ifndef NDF_EXP_NOPROD
 #pragma unroll
         for (int g = 0; g < 3; ++g)
@@ -1189,9 +1198,19 @@ query_pp_kernel(const TcArgs t) {
           named_bar(9 + s, 256);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
           if (ch == 0) {
-            const int64_t vloc = (first + kk * tile_stride) * kTileM + wtid;
+            const int64_t tile_g = first + kk * tile_stride;
+            const int64_t r = t.n_ref == 1 ? 0 : (int64_t)((uint32_t)tile_g / (uint32_t)n_vt);
+            const int64_t vloc = (tile_g - r * n_vt) * kTileM + wtid;
             const float z = part + dotx[s * kTileM + wtid] + bias_out;
-            if (vloc < n) a.out[vloc] = head_exact(a.m.head, z);
+            if (vloc < n) {
+              const float o = head_exact(a.m.head, z);
+              if (t.out16) {
+                const __half ho = __float2half_rn(o);
+                t.out16[r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&ho);
+              } else {
+                a.out[vloc] = o;
+              }
+            }
           }
           named_bar(9 + s, 256);                      // dotx consumed before the next tile
           NDF_TRACE_AT((int)kk, 6);
@@ -1271,18 +1290,23 @@ __device__ __forceinline__ void axis_features(double p, float* f) {
 //             (fp32; the query branch's grid)
 // Same fp64 operations as embed_point_t, so every feature has the same bits; one
 // sincos per thread keeps the fp64 latency chain short.
-__global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_lat, float* lz) {
+// refs: n_ref x 3 fp64 device reference points (multi-reference cube), or NULL for
+// the single reference in a.ref.  Nodes: nx + ny + nz query axis nodes, then 3 per
+// reference; the reference latent channels go to eref_lat + r * kERefStride.
+__global__ void prep_ws_feat_kernel(const QueryArgs a, const double* refs, int n_ref, float* feat,
+                                    float* eref_lat, float* lz) {
   asm volatile("griddepcontrol.launch_dependents;");
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int nnode = a.nx + a.ny + a.nz + 3;
+  const int nq = a.nx + a.ny + a.nz;
+  const int nnode = nq + 3 * n_ref;
   const int64_t F = (int64_t)nnode * kL;
   if (tid < F) {
     const int node = (int)(tid / kL), o = (int)(tid % kL);
     double p;
     if (node < a.nx) p = node_coord(node, a.nx);
     else if (node < a.nx + a.ny) p = node_coord(node - a.nx, a.ny);
-    else if (node < a.nx + a.ny + a.nz) p = node_coord(node - a.nx - a.ny, a.nz);
-    else p = a.ref[node - (a.nx + a.ny + a.nz)];
+    else if (node < nq) p = node_coord(node - a.nx - a.ny, a.nz);
+    else p = refs ? refs[node - nq] : a.ref[node - nq];
     p = fmin(fmax(p, -1.0), 1.0);
     double scale = 3.141592653589793;
     for (int i = 0; i < o; ++i) scale = scale * 2.0;
@@ -1292,10 +1316,12 @@ __global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_
     f[1 + 2 * o] = (float)sn;
     f[2 + 2 * o] = (float)cs;
     if (o == 0) f[0] = (float)p;
-  } else if (tid == F) {
+  } else if (tid < F + n_ref) {
+    const int r = (int)(tid - F);
+    const double* rp = refs ? refs + 3 * r : a.ref;
     const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
-    const double p[3] = {fmin(fmax(a.ref[0], -1.0), 1.0), fmin(fmax(a.ref[1], -1.0), 1.0),
-                         fmin(fmax(a.ref[2], -1.0), 1.0)};
+    const double p[3] = {fmin(fmax(rp[0], -1.0), 1.0), fmin(fmax(rp[1], -1.0), 1.0),
+                         fmin(fmax(rp[2], -1.0), 1.0)};
     const AxisCoord cx = level_coord(p[0], a.g.rx);
     const AxisCoord cy = level_coord(p[1], a.g.ry);
     const AxisCoord cz = level_coord(p[2], a.g.rz);
@@ -1313,9 +1339,9 @@ __global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_
       for (int ch = 0; ch < kC; ++ch)
         acc[ch] = dadd(acc[ch], dmul(w, (double)__ldg(grid + (size_t)idx * kC + ch)));
     }
-    for (int ch = 0; ch < kC; ++ch) eref_lat[ch] = (float)acc[ch];
+    for (int ch = 0; ch < kC; ++ch) eref_lat[(size_t)r * kERefStride + ch] = (float)acc[ch];
   } else {
-    const int64_t k = tid - F - 1;
+    const int64_t k = tid - F - n_ref;
     if (k >= (int64_t)a.nz * a.g.ry * a.g.rx) return;
     const int cx = (int)(k % a.g.rx), cy = (int)((k / a.g.rx) % a.g.ry);
     const int iz = (int)(k / ((int64_t)a.g.rx * a.g.ry));
@@ -1341,13 +1367,21 @@ __global__ void prep_ws_feat_kernel(const QueryArgs a, float* feat, float* eref_
 //   [0, nx)             xtab[ix]   = Fourier-x words 0..11, raw-x word at 12
 //   [nx, nx + ny*nz)    yztab[row] = Fourier-(y, z) words in A order, raw y, z at 24, 25
 template <bool F16>
-__global__ void prep_ws_merge_kernel(const QueryArgs a, const float* __restrict__ feat,
+// Per reference r: nx x-rows then ny*nz (y, z)-rows, tables of reference r at
+// xtab + r * nx * kXTabWords and yztab + r * ny * nz * kYZTabWords.
+__global__ void prep_ws_merge_kernel(const QueryArgs a, int n_ref, const float* __restrict__ feat,
                                      uint32_t* xtab, uint32_t* yztab) {
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");      // feat from prep_ws_feat_kernel
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nyz = a.ny * a.nz;
-  const int nref = a.nx + a.ny + a.nz;          // first reference node
+  const int64_t rows = (int64_t)a.nx + nyz;
+  if (gtid >= rows * n_ref) return;
+  const int r = (int)(gtid / rows);
+  const int64_t tid = gtid - (int64_t)r * rows;
+  const int nref = a.nx + a.ny + a.nz + 3 * r;  // first node of reference r
+  xtab += (size_t)r * a.nx * kXTabWords;
+  yztab += (size_t)r * nyz * kYZTabWords;
   auto merged = [](float r, float q) { return pack2<F16>(r + q, fabsf(r - q)); };
   if (tid < a.nx) {
     const float* r = feat + (size_t)nref * 16;
@@ -1478,32 +1512,34 @@ static bool use_ws(const QueryArgs& a, int n_ref, int nwg) {
     const char* e = getenv("NDF_TC_SCHEDULE");
     classic = (e && e[0] == 'c') ? 1 : 0;
   }
-  return !classic && nwg == 4 && a.mode == 0 && n_ref == 1 && a.m.merge == NDF_MERGE_SUM_ABSDIFF;
+  (void)n_ref;
+  return !classic && nwg == 4 && a.mode == 0 && a.m.merge == NDF_MERGE_SUM_ABSDIFF;
 }
 
 template <bool F16, bool SILU, int KIND>
-static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, bool ws,
-                       cudaStream_t s) {
-  static SmemAttrCache attr_tc, attr_pp;
-  NDF_CUDA_CHECK(attr_tc.ensure(tc::query_tc_kernel<F16, SILU, KIND>, smem));
-  if constexpr (KIND == tc::kGridSingle)
-    NDF_CUDA_CHECK(attr_pp.ensure(tc::query_pp_kernel<F16, SILU>, smem));
-  if constexpr (KIND != tc::kGridSingle) {
-    tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
-  } else if (!ws) {
-    tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
-  } else {
-    // ping-pong: 2 slots x (epilogue + producer warpgroup) per CTA, one CTA per SM
-    const int64_t n = t.q.v1 - t.q.v0;
-    const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
-    const unsigned g2 = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));
-    const tc::Layout lay = tc::make_layout(t.q.m);
-    const size_t smem_pp = (size_t)((lay.blob_bytes + 1023) & ~1023) +
-                           (size_t)tc::kPPSlots * tc::kABytes +
-                           (size_t)(1 + lay.H) * tc::kBiasBlk + 2048;
-    NDF_CUDA_CHECK(launch_pdl(tc::query_pp_kernel<F16, SILU>, g2, tc::kPPThreads, smem_pp, s, t));
-  }
+static int launch_tc_t(const tc::TcArgs& t, int nwg, size_t smem, unsigned grid, cudaStream_t s) {
+  static SmemAttrCache attr;
+  NDF_CUDA_CHECK(attr.ensure(tc::query_tc_kernel<F16, SILU, KIND>, smem));
+  tc::query_tc_kernel<F16, SILU, KIND><<<grid, nwg * 128, smem, s>>>(t, nwg);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+// ping-pong: 2 slots x (epilogue + producer warpgroup) per CTA, one CTA per SM;
+// t.n_ref references (single query or multi-reference cube)
+template <bool F16, bool SILU>
+static int launch_pp_t(const tc::TcArgs& t, cudaStream_t s) {
+  const int64_t n = t.q.v1 - t.q.v0;
+  const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM * t.n_ref;
+  const unsigned g2 = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));
+  const tc::Layout lay = tc::make_layout(t.q.m);
+  const size_t smem_pp = (size_t)((lay.blob_bytes + 1023) & ~1023) +
+                         (size_t)tc::kPPSlots * tc::kABytes +
+                         (size_t)(1 + lay.H) * tc::kBiasBlk + 2048;
+  static SmemAttrCache attr;
+  NDF_CUDA_CHECK(attr.ensure(tc::query_pp_kernel<F16, SILU>, smem_pp));
+  NDF_CUDA_CHECK(launch_pdl(tc::query_pp_kernel<F16, SILU>, g2, tc::kPPThreads, smem_pp, s, t));
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }
@@ -1514,14 +1550,15 @@ static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned
   using namespace tc;
   const bool silu = t.q.m.activation == NDF_ACT_SILU;
   const int kind = t.q.mode == 1 ? kPoints : (t.n_ref > 1 ? kGridMulti : kGridSingle);
+  if (ws) return silu ? launch_pp_t<F16, true>(t, s) : launch_pp_t<F16, false>(t, s);
   if (silu) {
-    if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, ws, s);
-    if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, false, s);
-    return launch_tc_t<F16, true, kPoints>(t, nwg, smem, grid, false, s);
+    if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, s);
+    if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, s);
+    return launch_tc_t<F16, true, kPoints>(t, nwg, smem, grid, s);
   }
-  if (kind == kGridSingle) return launch_tc_t<F16, false, kGridSingle>(t, nwg, smem, grid, ws, s);
-  if (kind == kGridMulti) return launch_tc_t<F16, false, kGridMulti>(t, nwg, smem, grid, false, s);
-  return launch_tc_t<F16, false, kPoints>(t, nwg, smem, grid, false, s);
+  if (kind == kGridSingle) return launch_tc_t<F16, false, kGridSingle>(t, nwg, smem, grid, s);
+  if (kind == kGridMulti) return launch_tc_t<F16, false, kGridMulti>(t, nwg, smem, grid, s);
+  return launch_tc_t<F16, false, kPoints>(t, nwg, smem, grid, s);
 }
 
 // Grid / points query on the tensor cores; refs (device, n_ref x 3) and out16 are
@@ -1572,15 +1609,17 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
                 "tensor-core grid query supports < 2^32 vertices");
     const int threads = 128;
     if (ws) {
-      // per-query tables: axis features, x words, (y, z) words, z-interpolated
-      // latent rows, reference latent channels
+      NDF_REQUIRE((a.v1 - a.v0 + tc::kTileM - 1) / tc::kTileM * n_ref < (1LL << 32),
+                  NDF_ERR_UNSUPPORTED, "too many reference x vertex tiles for one launch");
+      // per-query tables: axis features, x words and (y, z) words per reference,
+      // z-interpolated latent rows, reference latent channels
       const int64_t nyz = (int64_t)a.ny * a.nz;
-      const int nnode = a.nx + a.ny + a.nz + 3;
+      const int nnode = a.nx + a.ny + a.nz + 3 * n_ref;
       const size_t fb = (size_t)nnode * 16 * 4;
-      const size_t xb = (size_t)a.nx * tc::kXTabWords * 4;
-      const size_t yb = (size_t)nyz * tc::kYZTabWords * 4;
+      const size_t xb = (size_t)n_ref * a.nx * tc::kXTabWords * 4;
+      const size_t yb = (size_t)n_ref * nyz * tc::kYZTabWords * 4;
       const size_t lb = (size_t)a.nz * a.g.ry * a.g.rx * tc::kC * 4;
-      const size_t eb = (size_t)tc::kERefStride * 4;
+      const size_t eb = (size_t)n_ref * tc::kERefStride * 4;
       NDF_CUDA_CHECK(scratch_alloc(&scratch, fb + xb + yb + lb + eb + 256, s));
       uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
       float* feat = reinterpret_cast<float*>(p);
@@ -1592,15 +1631,18 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
       t.yztab = yt;
       t.lz = lt;
       t.erefs = et;
-      const int64_t n1 = (int64_t)nnode * tc::kL + 1 + (int64_t)a.nz * a.g.ry * a.g.rx;
-      tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(a, feat, et, lt);
+      const int64_t n1 = (int64_t)nnode * tc::kL + n_ref + (int64_t)a.nz * a.g.ry * a.g.rx;
+      tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(
+          a, refs_dev, n_ref, feat, et, lt);
       NDF_LAUNCH_CHECK();
-      const unsigned b2 = (unsigned)((a.nx + nyz + 255) / 256);
+      const unsigned b2 = (unsigned)(((a.nx + nyz) * n_ref + 255) / 256);
       const float* featc = feat;
       if (a.prec == NDF_PREC_FP16)
-        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<true>, b2, 256, 0, s, a, featc, xt, yt));
+        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<true>, b2, 256, 0, s, a, n_ref, featc,
+                                  xt, yt));
       else
-        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<false>, b2, 256, 0, s, a, featc, xt, yt));
+        NDF_CUDA_CHECK(launch_pdl(tc::prep_ws_merge_kernel<false>, b2, 256, 0, s, a, n_ref, featc,
+                                  xt, yt));
       NDF_LAUNCH_CHECK();
     } else {
       const int naxis = a.nx + a.ny + a.nz;

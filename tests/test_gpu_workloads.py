@@ -19,21 +19,25 @@ from paper_2307_02203_b200 import workloads as W  # noqa: E402
 
 
 @pytest.mark.parametrize("precision", ["fp16", "bf16"])
-def test_multi_reference_cube_equals_single_queries(precision):
+@pytest.mark.parametrize("merge", ["sum_absdiff", "add"])
+def test_multi_reference_cube_equals_single_queries(precision, merge):
+    """The cube row of a reference is its single query rounded to fp16, bit for bit:
+    sum_absdiff runs both on the ping-pong kernel (per-reference tables), the other
+    merges both on the classic schedule (query embedding reused across references)."""
+    from dataclasses import replace
     dims = (70, 40, 6)
     spec = ndf.ModelSpec.baseline(dims, 4, precision=precision, grid_init=1.0)
+    if merge != "sum_absdiff":
+        spec = replace(spec, merge=merge)
     model = ndf.NdfModel.build(spec, seed=3)
     rng = np.random.default_rng(0)
     refs = np.concatenate([rng.uniform(-1, 1, (5, 3)), [[-1.0, 1.0, 0.2]]])
     V = int(np.prod(dims))
     cube = ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims).cpu()
     assert cube.shape == (len(refs), V) and cube.dtype == torch.float16
-    # single-reference queries run the warp-specialised schedule (table-fed encoder,
-    # fp32 output dot product), the cube the classic one: equal within 16-bit precision
-    tol = 4e-3 if precision == "fp16" else 1.5e-2
     for r, ref in enumerate(refs):
         single = ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, dims).cpu()
-        assert float((cube[r].float() - single).abs().max()) <= tol
+        assert torch.equal(cube[r], single.half()), (merge, r)
     # vertex sub-range into a strided output
     out = torch.zeros((len(refs), 2000), dtype=torch.float16, device="cuda")
     ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims, 1000, 2500, out=out)
