@@ -12,14 +12,15 @@
 // exact in 16-bit, so silu(x) = y + y tanh(y) with y = x/2: one MUFU tanh and one
 // FMA per element):
 //
-// * query_pp_kernel (default for single-reference grid queries, the BASELINE hot
-//   path): per CTA two "slots" of 128 query vertices, each with two TMEM accumulator
+// * query_pp_kernel (default for grid queries with the sum_absdiff merge -- the
+//   BASELINE hot path, single reference or multi-reference cube): per CTA two "slots"
+//   of 128 query vertices, each with two TMEM accumulator
 //   halves so layer l+1's MMAs run underneath layer l's epilogue, hidden-layer A
 //   operands taken straight from TMEM, dedicated producer and MMA-issuer warps, and
 //   the output layer as an fp32 dot product.  See the comment above the kernel.
 //
-// * query_tc_kernel ("classic"; multi-reference cubes, paired/points forward, the
-//   reference's other merges): one CTA per SM with up to 4 symmetric warpgroups,
+// * query_tc_kernel ("classic"; paired/points forward and the reference's other
+//   merges, single or multi-reference): one CTA per SM with up to 4 symmetric warpgroups,
 //   each owning a 128-row tile, one 32 KB SMEM A buffer (SWIZZLE_NONE canonical:
 //   8x16 B core matrices, LBO = 128 B along K, SBO = 2048 B along M) and 128 TMEM
 //   columns (row m of the tile = TMEM lane m = thread m of the warpgroup); one thread
