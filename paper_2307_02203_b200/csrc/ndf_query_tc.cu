@@ -879,8 +879,11 @@ __device__ __forceinline__ void dot16(const float* x, int c0, int act, uint32_t 
           dots[(i & 3) + 1]);
 }
 
-// Ping-pong schedule for single-reference grid queries (sum_absdiff merge; the
-// default -- NDF_TC_SCHEDULE=classic selects query_tc_kernel instead).
+// Ping-pong schedule for grid queries with the sum_absdiff merge (the default --
+// NDF_TC_SCHEDULE=classic selects query_tc_kernel instead).  A launch covers t.n_ref
+// references: tile T is vertex tile T mod n_vt of reference T / n_vt, with that
+// reference's x / (y, z) tables and latent channels; rows go to out (fp32, single
+// reference) or out16 (fp16 cube rows of ld_out).
 //   2 slots per CTA, each = 256 TMEM columns holding TWO accumulator halves plus a
 //   32 KB SMEM buffer for layer 0's A operand.  Layer l of a slot accumulates into
 //   half (l & 1) while the epilogue drains the other half, so the next layer's MMA
