@@ -42,6 +42,9 @@ def test_multi_reference_cube_equals_single_queries(precision, merge):
     out = torch.zeros((len(refs), 2000), dtype=torch.float16, device="cuda")
     ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, dims, 1000, 2500, out=out)
     assert torch.equal(out[:, :1500].cpu(), cube[:, 1000:2500])
+    # a one-reference cube through the multi-reference entry point
+    one = ndf.reconstruct_multi_device(model, refs[2:3], ndf.ROLE_MU, dims).cpu()
+    assert torch.equal(one[0], cube[2])
 
 
 def test_multi_reference_oracle_spot_check():
