@@ -4,8 +4,8 @@
 ``matrix_reconstruct`` (:97-125) and ``benchmark`` (:186-220) with the
 reference's signatures.  The query runs as ONE kernel launch over the whole
 output grid: the reference point is embedded once per CTA, every query vertex
-once, and the decoder runs fused on the tensor cores (bf16 models) or in exact
-fp32 (fp32 models).  ``batch_size`` is accepted for signature compatibility;
+once, and the decoder runs fused on the tensor cores (fp16 / bf16 models) or in
+exact fp32 (fp32 models).  ``batch_size`` is accepted for signature compatibility;
 per-row arithmetic never depends on batching, so results are identical for any
 value -- the property the reference guarantees (service.py:52-54).
 """
@@ -206,9 +206,11 @@ def reconstruct_multi_device(model: NdfModel, refs, role: str = ROLE_MU, dims=(6
     """Dependence cube of several reference points: fp16 CUDA tensor (n_ref, v1 - v0).
 
     BASELINE config 3 (64 references x 1.76 M vertices per model).  The batched
-    form of the reference's per-reference loop (service.py:97-125): each query
-    vertex is embedded once and reused for every reference; values equal the
-    single-reference query's fp32 result rounded to fp16.
+    form of the reference's per-reference loop (service.py:97-125), one launch:
+    sum_absdiff models run the ping-pong kernel over reference x vertex tiles with
+    per-reference feature tables, the other merges embed each query vertex once and
+    reuse it for every reference.  Row r equals the single-reference query of
+    refs[r] rounded to fp16, bit for bit.
     """
     import torch
     _check_role(role)
