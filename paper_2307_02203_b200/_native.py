@@ -15,7 +15,9 @@ import threading
 from .errors import ConfigError, DeviceError, ParameterError, ShapeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libndf_b200.so")
+# NDF_LIB_PATH points timing experiments at a variant build (tools/build_variants.sh)
+# without touching the product library next to this file.
+LIB_PATH = os.environ.get("NDF_LIB_PATH") or os.path.join(HERE, "libndf_b200.so")
 
 NDF_MAX_LAYERS = 8
 NDF_MAX_WIDTH = 256

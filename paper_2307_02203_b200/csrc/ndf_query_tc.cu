@@ -188,6 +188,33 @@ __device__ __forceinline__ float merged_value(int merge_rt, int c, FA ea, FB eb)
   return 0.0f;
 }
 
+// Split an fp32 pair into bf16 hi / lo words: hi = bf16(x), lo = bf16(x - hi); the
+// difference is exact in fp32 (at most 16 significant bits).
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  hi = pack2<false>(x0, x1);
+  const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xffff0000u);
+  float l0, l1;
+  ffma2(l0, l1, h0, h1, -1.0f, -1.0f, x0, x1);       // x - hi, exact
+  lo = pack2<false>(l0, l1);
+}
+
+// 8 consecutive K values of one row of a 16-bit A operand; bf16 (!F16) writes the hi
+// plane at abase and the lo plane (x - bf16(x)) at abase + kABytes: the MMAs then run
+// A_hi W + A_lo W.
+template <bool F16>
+__device__ __forceinline__ void store_a8(uint32_t abase, int row, int k, const float* x) {
+  if constexpr (F16) {
+    st_shared_v4(abase + canon_off(row, k, kSboA), pack2<true>(x[0], x[1]), pack2<true>(x[2], x[3]),
+                 pack2<true>(x[4], x[5]), pack2<true>(x[6], x[7]));
+  } else {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_pair(x[2 * i], x[2 * i + 1], h[i], l[i]);
+    st_shared_v4(abase + canon_off(row, k, kSboA), h[0], h[1], h[2], h[3]);
+    st_shared_v4(abase + kABytes + canon_off(row, k, kSboA), l[0], l[1], l[2], l[3]);
+  }
+}
+
 template <bool F16, int MERGE, class FA, class FB>
 __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int merge, FA ea, FB eb,
                                                 int kin) {
@@ -197,8 +224,7 @@ __device__ __forceinline__ void write_input_row(uint32_t abase, int row, int mer
       float x[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] = merged_value<MERGE>(merge, 8 * kg + j, ea, eb);
-      st_shared_v4(abase + canon_off(row, kg * 8, kSboA), pack2<F16>(x[0], x[1]),
-                   pack2<F16>(x[2], x[3]), pack2<F16>(x[4], x[5]), pack2<F16>(x[6], x[7]));
+      store_a8<F16>(abase, row, kg * 8, x);
     }
   }
 }
@@ -478,6 +504,11 @@ struct TcArgs {
   long long* trace;       // debug: per-phase clock64 stamps of CTA 0 (NULL = off)
   int stagger;            // cycles between warpgroup start times (de-phases the WGs)
   int tokens;             // max warpgroups in an epilogue at once (0 = unlimited)
+  const void* px;         // x3 schedule: per-reference PX / PYZ layer-0 tables
+  const void* pyz;
+  int ngx, ngyz;          //   4-node groups per reference in px / pyz
+  int x3_wlo_mask;        //   bit l: hidden layer l runs the A_hi x W_lo term
+  int x3_burst;           //   1: issue a hidden layer's MMAs after its whole epilogue
 };
 
 // debug tracing of CTA 0's schedule: slot = (wg, tile#, event)
@@ -510,14 +541,18 @@ constexpr int kTraceBase = 6 * kTraceTiles * kTraceEvents;   // + 16 chunk stamp
 // One MMA stage: K/16 tcgen05.mma steps into the warpgroup's accumulator, committed
 // to its mbarrier.  Issued by one thread.
 // acc_first = 1: the accumulator was pre-loaded (bias) and every step accumulates.
+// split: the A operand has a lo plane at a_addr + kABytes (bf16 path), issued as a
+// second pass of K/16 steps against the same B.
 __device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr,
                                             int K, uint32_t sbo_b, uint32_t idesc, uint64_t* bar,
-                                            uint32_t acc_first) {
+                                            uint32_t acc_first, bool split = false) {
   tc_fence_after();
-  for (int kk = 0; kk < K / 16; ++kk) {
-    const uint64_t ad = smem_desc(a_addr + kk * 256, 128, kSboA);
-    const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
-    mma_bf16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : acc_first);
+  for (int p = 0; p < (split ? 2 : 1); ++p) {
+    for (int kk = 0; kk < K / 16; ++kk) {
+      const uint64_t ad = smem_desc(a_addr + p * kABytes + kk * 256, 128, kSboA);
+      const uint64_t bd = smem_desc(b_addr + kk * 256, 128, sbo_b);
+      mma_bf16(d_tmem, ad, bd, idesc, (kk > 0 || p > 0) ? 1u : acc_first);
+    }
   }
   mma_commit(bar);
 }
@@ -535,7 +570,8 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   const Layout lay = make_layout(a.m);
   uint8_t* wblob = smem;                                   // parameter blob
   uint8_t* abufs = smem + ((lay.blob_bytes + 1023) & ~1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + nwg * kABytes);   // [0] weights, [1+w]
+  constexpr int kAPer = F16 ? kABytes : 2 * kABytes;   // bf16: hi and lo planes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(abufs + nwg * kAPer);     // [0] weights, [1+w]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   float* eref_s = reinterpret_cast<float*>(bars + 16);      // single-ref grid: e_ref in SMEM
   int* epi_tok = reinterpret_cast<int*>(bars + 64);          // epilogue admission counter
@@ -571,7 +607,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t d_tmem = tmem_base + (uint32_t)(wg * kHid);       // column offset
   const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;    // TMEM lane quarter
-  const uint32_t a_addr = smem_u32(abufs + wg * kABytes);
+  const uint32_t a_addr = smem_u32(abufs + wg * kAPer);
   const uint32_t tmem_row = tmem_base + lane_base + (uint32_t)(wg * kHid);  // this thread's lane
   const uint32_t w_addr = smem_u32(wblob);
   uint64_t* bar = &bars[1 + wg];
@@ -669,7 +705,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         if (wtid == 0) {
           const uint32_t wl = w_addr + (l == 0 ? 0 : lay.w0_bytes + (l - 1) * lay.wh_bytes);
           issue_stage(d_tmem, a_addr, wl, l == 0 ? lay.kin : kHid, l == 0 ? sbo_w0 : kSboA,
-                      idesc, bar, 1u);
+                      idesc, bar, 1u, !F16);
         }
         mbar_wait(bar, phase);
         phase ^= 1;
@@ -723,10 +759,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
             for (int i = 0; i < 32; ++i) h[i] = act_f32(a.m.activation, v[i]);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(a_addr + canon_off(wtid, c0 + 8 * j, kSboA),
-                         pack2<F16>(h[8 * j], h[8 * j + 1]), pack2<F16>(h[8 * j + 2], h[8 * j + 3]),
-                         pack2<F16>(h[8 * j + 4], h[8 * j + 5]), pack2<F16>(h[8 * j + 6], h[8 * j + 7]));
+          for (int j = 0; j < 4; ++j) store_a8<F16>(a_addr, wtid, c0 + 8 * j, h + 8 * j);
           NDF_CHUNK_TRACE(3);
         }
         if (next_hidden) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -737,18 +770,21 @@ query_tc_kernel(const TcArgs t, const int nwg) {
         NDF_TRACE(3 + 2 * l);
       }
       // ---- output layer (128 -> 1) as a 16-column MMA ---------------------------------
+      // bf16: column 3 of the output MMA is A . w_lo (packed into row 3 of the operand)
       if (wtid == 0)
-        issue_stage(d_tmem, a_addr, w_addr + lay.wout_off, kHid, kSboA, idesc_out, bar, 0u);
+        issue_stage(d_tmem, a_addr, w_addr + lay.wout_off, kHid, kSboA, idesc_out, bar, 0u, !F16);
       mbar_wait(bar, phase);
       phase ^= 1;
       tc_fence_after();
       NDF_TRACE(10);
-      uint32_t zr;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                   : "=r"(zr) : "r"(tmem_row));
+      uint32_t zr, z1, z2, z3;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(zr), "=r"(z1), "=r"(z2), "=r"(z3) : "r"(tmem_row));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      (void)z1; (void)z2;
       if (valid) {
-        const float z = head_exact(a.m.head, __uint_as_float(zr) + bias_out);
+        const float zo = F16 ? __uint_as_float(zr) : __uint_as_float(zr) + __uint_as_float(z3);
+        const float z = head_exact(a.m.head, zo + bias_out);
         if (t.out16) {
           const __half hz = __float2half_rn(z);
           t.out16[(size_t)r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&hz);
@@ -1230,6 +1266,8 @@ query_pp_kernel(const TcArgs t) {
                  "r"(512));
 }
 
+#include "ndf_query_x3.cuh"
+
 // ---- per-query prep: per-axis Fourier table + reference embeddings ------------
 __global__ void prep_kernel(const QueryArgs a, const double* refs, int n_ref, float* ftab,
                             float* erefs) {
@@ -1461,6 +1499,10 @@ __global__ void pack_fill_kernel(const ndf_model_desc m, uint8_t* blob) {
         // fp32 copy in rows 1-2 (output columns 1..15 of the N=16 MMA are never read):
         // k-group g's 8 weights at g*128 + 16 (query_pp_kernel's output dot product)
         *reinterpret_cast<float*>(blob + lay.wout_off + (e >> 3) * 128 + 16 + (e & 7) * 4) = W[e];
+        // bf16: lo part in row 3 (the classic kernel's output MMA reads column 3)
+        if (!f16)
+          store16(blob + lay.wout_off + canon_off(3, (int)e, kSboA),
+                  W[e] - __bfloat162float(__float2bfloat16_rn(W[e])), false);
       }
       if (gtid == 0) vecs[lay.H * kHid] = b[0];
     }
@@ -1501,23 +1543,30 @@ static bool tc_supported(const ndf_model_desc& m, std::string* why) {
     if (m.widths[i] != tc::kHid) return fail("tcgen05 path needs hidden width 128");
   if (m.widths[m.n_layers] != 1) return fail("decoder must emit one scalar");
   const tc::Layout lay = tc::make_layout(m);
-  if (((lay.blob_bytes + 1023) & ~1023) + tc::kABytes + 1024 > tc::kMaxSmem)
+  const int a_per_wg = m.tc_format == NDF_PREC_BF16 ? 2 * tc::kABytes : tc::kABytes;
+  if (((lay.blob_bytes + 1023) & ~1023) + a_per_wg + 1024 > tc::kMaxSmem)
     return fail("too many hidden layers for the SMEM-resident weights");
   return true;
+}
+
+static bool tc_schedule_classic() {
+  static int classic = -1;
+  if (classic < 0) {
+    const char* e = getenv("NDF_TC_SCHEDULE");
+    classic = (e && e[0] == 'c') ? 1 : 0;
+  }
+  return classic == 1;
 }
 
 // Schedule for single-reference grid queries with the sum_absdiff merge: "ws"
 // (default; 4 epilogue + 2 producer warpgroups fed by per-query x / (y, z) tables)
 // or "classic" (4 symmetric warpgroups doing everything; also used for points,
 // multi-reference queries and the other merges).  NDF_TC_SCHEDULE=classic forces it.
+// fp16 only: bf16 grid queries of this family run the split-operand query_x3_kernel.
 static bool use_ws(const QueryArgs& a, int n_ref, int nwg) {
-  static int classic = -1;
-  if (classic < 0) {
-    const char* e = getenv("NDF_TC_SCHEDULE");
-    classic = (e && e[0] == 'c') ? 1 : 0;
-  }
   (void)n_ref;
-  return !classic && nwg == 4 && a.mode == 0 && a.m.merge == NDF_MERGE_SUM_ABSDIFF;
+  return !tc_schedule_classic() && a.prec == NDF_PREC_FP16 && nwg == 4 && a.mode == 0 &&
+         a.m.merge == NDF_MERGE_SUM_ABSDIFF;
 }
 
 template <bool F16, bool SILU, int KIND>
@@ -1554,7 +1603,9 @@ static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned
   using namespace tc;
   const bool silu = t.q.m.activation == NDF_ACT_SILU;
   const int kind = t.q.mode == 1 ? kPoints : (t.n_ref > 1 ? kGridMulti : kGridSingle);
-  if (ws) return silu ? launch_pp_t<F16, true>(t, s) : launch_pp_t<F16, false>(t, s);
+  if constexpr (F16) {
+    if (ws) return silu ? launch_pp_t<true, true>(t, s) : launch_pp_t<true, false>(t, s);
+  }
   if (silu) {
     if (kind == kGridSingle) return launch_tc_t<F16, true, kGridSingle>(t, nwg, smem, grid, s);
     if (kind == kGridMulti) return launch_tc_t<F16, true, kGridMulti>(t, nwg, smem, grid, s);
@@ -1569,6 +1620,86 @@ static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned
 // only used by the multi-reference entry point.
 static long long* g_trace = nullptr;   // debug hook (ndf_debug_tc_trace)
 
+// bf16 grid query on the split-operand kernel: prep_ws_feat_kernel (axis features,
+// reference latent channels, z-interpolated latent rows) -> prep_x3_tab_kernel (PX / PYZ
+// layer-0 tables per reference) -> query_x3_kernel, chained by programmatic dependent
+// launch.  NDF_X3_WLO (bitmask of hidden layers, default all) selects which hidden
+// layers run the A_hi x W_lo term -- a timing / accuracy experiment knob.
+static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t s) {
+  const QueryArgs& a = t.q;
+  static int wlo = -1;
+  if (wlo < 0) {
+    const char* e = getenv("NDF_X3_WLO");
+    wlo = e ? (int)strtol(e, nullptr, 0) : 0xff;
+  }
+  t.x3_wlo_mask = wlo;
+  static int burst = -1;
+  if (burst < 0) {
+    const char* e = getenv("NDF_X3_BURST");
+    burst = e ? atoi(e) : 0;
+  }
+  t.x3_burst = burst;
+  const int nnode = a.nx + a.ny + a.nz + 3 * n_ref;
+  const int ngx = (a.nx + tc::kX3TX - 1) / tc::kX3TX * 2;
+  const tc::X3Tiles tg = tc::x3_tiles(a.nx, a.v0, a.v1);
+  const int64_t ngyz64 = tg.n_vt / (tg.n_xt) * 4;        // row-tiles of this launch x 4 groups
+  NDF_REQUIRE(ngyz64 < (1LL << 30), NDF_ERR_UNSUPPORTED, "too many (y, z) rows for the bf16 path");
+  const int ngyz = (int)ngyz64;
+  NDF_REQUIRE((int64_t)n_ref * (ngx + ngyz) < (1LL << 31), NDF_ERR_UNSUPPORTED,
+              "too many reference x table groups for one bf16 launch");
+  const size_t fb = ((size_t)nnode * 16 * 4 + 255) & ~(size_t)255;
+  const size_t lb = ((size_t)a.nz * a.g.ry * a.g.rx * tc::kC * 4 + 255) & ~(size_t)255;
+  const size_t eb = ((size_t)n_ref * tc::kERefStride * 4 + 255) & ~(size_t)255;
+  const size_t xb = (size_t)n_ref * ngx * tc::kX3Blk;
+  const size_t yb = (size_t)n_ref * ngyz * tc::kX3Blk;
+  void* scratch = nullptr;
+  NDF_CUDA_CHECK(scratch_alloc(&scratch, fb + lb + eb + xb + yb, s));
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  float* feat = reinterpret_cast<float*>(p);
+  float* lt = reinterpret_cast<float*>(p + fb);
+  float* et = reinterpret_cast<float*>(p + fb + lb);
+  uint4* px = reinterpret_cast<uint4*>(p + fb + lb + eb);
+  uint4* pyz = reinterpret_cast<uint4*>(p + fb + lb + eb + xb);
+  t.lz = lt;
+  t.erefs = et;
+  t.px = px;
+  t.pyz = pyz;
+  t.ngx = ngx;
+  t.ngyz = ngyz;
+  int st = NDF_OK;
+  do {
+    const int64_t n1 = (int64_t)nnode * tc::kL + n_ref + (int64_t)a.nz * a.g.ry * a.g.rx;
+    tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(a, refs_dev, n_ref, feat,
+                                                                          et, lt);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    const float* featc = feat;
+    if (e == cudaSuccess)
+      e = launch_pdl(tc::prep_x3_tab_kernel, (unsigned)((int64_t)n_ref * (ngx + ngyz)), 128, 0, s, a, n_ref,
+                     featc, ngx, ngyz, (int64_t)tg.ty0 * tc::kX3TY, px, pyz);
+    count_launch();
+    const int64_t tiles = tg.n_vt * n_ref;
+    const unsigned g2 = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));
+    const size_t smem = (size_t)tc::make_x3_layout(a.m).smem_total;
+    const bool silu = a.m.activation == NDF_ACT_SILU;
+    static SmemAttrCache attr_s, attr_g;
+    if (e == cudaSuccess)
+      e = silu ? attr_s.ensure(tc::query_x3_kernel<true>, smem)
+               : attr_g.ensure(tc::query_x3_kernel<false>, smem);
+    if (e == cudaSuccess)
+      e = silu ? launch_pdl(tc::query_x3_kernel<true>, g2, tc::kPPThreads, smem, s, t)
+               : launch_pdl(tc::query_x3_kernel<false>, g2, tc::kPPThreads, smem, s, t);
+    count_launch();
+    if (e != cudaSuccess) {
+      set_error(std::string("bf16 query launch failed: ") + cudaGetErrorString(e));
+      st = NDF_ERR_CUDA;
+    }
+  } while (0);
+  cudaFreeAsync(scratch, s);
+  return st;
+}
+
 static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_t* out16,
                   int64_t ld_out, cudaStream_t s) {
   std::string why;
@@ -1579,8 +1710,9 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
               "packed blob element type does not match the requested precision");
   const tc::Layout lay = tc::make_layout(a.m);
   const int blob_al = (lay.blob_bytes + 1023) & ~1023;
-  const int nwg = std::min((tc::kMaxSmem - blob_al - 1024) / tc::kABytes, 4);
-  const size_t smem = (size_t)blob_al + (size_t)nwg * tc::kABytes + 1024;
+  const int a_per_wg = a.prec == NDF_PREC_BF16 ? 2 * tc::kABytes : tc::kABytes;
+  const int nwg = std::min((tc::kMaxSmem - blob_al - 1024) / a_per_wg, 4);
+  const size_t smem = (size_t)blob_al + (size_t)nwg * a_per_wg + 1024;
   const int64_t n = a.v1 - a.v0;
   const int64_t tiles = (n + tc::kTileM - 1) / tc::kTileM;
   const int64_t ctas = std::min<int64_t>((tiles + nwg - 1) / nwg, sm_count());
@@ -1611,6 +1743,7 @@ static int run_tc(const QueryArgs& a, const double* refs_dev, int n_ref, uint16_
   if (a.mode == 0) {
     NDF_REQUIRE((int64_t)a.nx * a.ny * a.nz < (1LL << 32), NDF_ERR_UNSUPPORTED,
                 "tensor-core grid query supports < 2^32 vertices");
+    if (!tc_schedule_classic() && tc::x3_supported(a.m)) return run_x3(t, refs_dev, n_ref, s);
     const int threads = 128;
     if (ws) {
       NDF_REQUIRE((a.v1 - a.v0 + tc::kTileM - 1) / tc::kTileM * n_ref < (1LL << 32),
@@ -1677,17 +1810,25 @@ using namespace ndf;
 // trace builds only, -DNDF_TRACE_BUILD).
 extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 
+// bf16 blobs of the BASELINE family carry the split-operand extension (X3Layout).
+static size_t tc_blob_total(const ndf_model_desc& m) {
+  if (tc::x3_supported(m)) {
+    const tc::X3Layout xl = tc::make_x3_layout(m);
+    return (size_t)xl.ext_off + (size_t)xl.ext_bytes;
+  }
+  return (size_t)tc::make_layout(m).blob_bytes;
+}
+
 extern "C" size_t ndf_tc_blob_bytes(const ndf_model_desc* m) {
   if (!m || !tc_supported(*m, nullptr)) return 0;
-  return (size_t)tc::make_layout(*m).blob_bytes;
+  return tc_blob_total(*m);
 }
 
 extern "C" int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_bytes, void* stream) {
   NDF_REQUIRE(m && blob, NDF_ERR_PARAMETER, "null pointer");
   std::string why;
   NDF_REQUIRE(tc_supported(*m, &why), NDF_ERR_UNSUPPORTED, why);
-  const tc::Layout lay = tc::make_layout(*m);
-  NDF_REQUIRE(blob_bytes >= (size_t)lay.blob_bytes, NDF_ERR_PARAMETER, "blob too small");
+  NDF_REQUIRE(blob_bytes >= tc_blob_total(*m), NDF_ERR_PARAMETER, "blob too small");
   NDF_REQUIRE((reinterpret_cast<uintptr_t>(blob) & 15) == 0, NDF_ERR_PARAMETER,
               "blob must be 16-byte aligned");
   NDF_REQUIRE(m->params_f32 != nullptr, NDF_ERR_PARAMETER, "null params_f32");
@@ -1697,6 +1838,10 @@ extern "C" int ndf_tc_pack(const ndf_model_desc* m, void* blob, size_t blob_byte
   NDF_LAUNCH_CHECK();
   tc::pack_fill_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
   NDF_LAUNCH_CHECK();
+  if (tc::x3_supported(*m)) {
+    tc::pack_x3_kernel<<<64, 256, 0, as_stream(stream)>>>(*m, (uint8_t*)blob);
+    NDF_LAUNCH_CHECK();
+  }
   return NDF_OK;
 }
 

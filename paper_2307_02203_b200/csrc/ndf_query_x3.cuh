@@ -1,0 +1,649 @@
+// bf16 grid query with split ("bf16x3") operands -- included by ndf_query_tc.cu inside
+// namespace ndf::tc (it reuses that file's helpers and the ping-pong warp roles).
+//
+// Why: plain bf16 operands (8 significant bits) put the decoder 1.2-1.4e-2 away from the
+// fp32 reference on the BASELINE model at config-1 scale -- outside the north_star's 1e-2
+// contract -- and NumPy simulation (tools/bf16_sim.py) shows the error is split between
+// the layer-0 inputs, the hidden activations and the weights.  This kernel removes all
+// three while every MMA stays a bf16 x bf16 -> fp32 tcgen05.mma:
+//
+// * Layer 0 is separable on the output grid: every embedding feature except the 16
+//   latent channels depends on x alone (raw x, Fourier-x) or on the (y, z) row alone
+//   (raw y/z, Fourier-y/z), so its pre-activation is
+//       z0 = PX[ix] + PYZ[iy, iz] + W_lat^T [r + lat, |r - lat|]
+//   with PX / PYZ (bias folded into PYZ) computed per query in fp64 by
+//   prep_x3_tab_kernel from the fp32 merged features and fp32 weights, stored as
+//   bf16 hi + lo pairs (16 significant bits).  A tile is 8 x-nodes x 16 (y, z)-rows,
+//   so PX and PYZ enter the accumulator through two constant one-hot selector blocks
+//   (A = [1 1] in the columns of the row's node, B = the tile's 8 PX / 16 PYZ rows,
+//   hi and lo): 3 K16 MMA steps, and each tile's B blocks are two contiguous bulk
+//   copies (4 KB + 8 KB) from the tables (LBO = 2048 B along K, SBO = 128 B along N).
+//   The latent words go hi/lo as well: A_hi W_hi + A_lo W_hi + A_hi W_lo (6 steps).
+// * Hidden layers: the epilogue writes each 16-column sub-chunk's activations as 8 hi
+//   words + 8 lo words (h - bf16(h) is exact in fp32) into the sub-chunk's own 16
+//   drained TMEM columns, and the issuer runs A_hi W_hi + A_lo W_hi + A_hi W_lo per
+//   K16 step (W_lo = bf16(w - bf16(w)) resident in SMEM).  The dropped A_lo W_lo term
+//   is 2^-18 relative.
+// * Biases of hidden layers: hi at k = 0, lo at k = 1 of the bias MMA step.
+// * Output layer: fp32 dot product in the last epilogue (fp32 weights), as before.
+// Remaining error: tanh.approx in SiLU and the 2^-17 representation error -- measured
+// against the fp32 oracle in tests/test_gpu_query.py (TOL_BF16 = 1e-2).
+//
+// Warp roles, TMEM slots and barriers are those of query_pp_kernel (see there); the
+// producer now only builds the 32 latent words, issues the two bulk copies and the 9
+// layer-0 MMAs; the issuer sends 3 MMAs per K16 step.
+
+constexpr int kX3TX = 8;                  // tile: 8 x-nodes ...
+constexpr int kX3TY = 16;                 // ... x 16 (y, z)-rows = 128 rows
+constexpr int kX3Blk = 128 * 16;          // one 8-K group of a 128-row operand (2 KB)
+constexpr int kX3SelX = 2 * kX3Blk;       // A selector for PX (K = 16)
+constexpr int kX3SelYZ = 4 * kX3Blk;      // A selector for PYZ (K = 32)
+constexpr int kX3Bx = 2 * kX3Blk;         // per slot: B = 8 PX rows (hi, lo)
+constexpr int kX3Byz = 4 * kX3Blk;        // per slot: B = 16 PYZ rows (hi, lo)
+constexpr int kX3ALat = 8 * kX3Blk;       // per slot: latent A, hi words K 0-31, lo 32-63
+constexpr int kX3Slot = kX3Bx + kX3Byz + kX3ALat;
+constexpr int kX3Lat = 3 + 6 * kL;        // first latent feature (39)
+constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0) in bf16
+
+// Extension of the packed bf16 blob, after the standard layout (make_layout):
+//   wlat_hi, wlat_lo: N=128 x K=32 (k = 2c + {0: sum, 1: absdiff} of latent channel c),
+//                     canonical K-major, SBO 512 B
+//   wh_lo[l-1]:       lo parts of hidden layers 1..H-1, same layout as their hi parts
+//   wout32:           output weights, fp32
+struct X3Layout {
+  int ext_off;
+  int wlat_hi, wlat_lo, wh_lo, wout32, ext_bytes;
+  int smem_w;      // resident weights: hidden W_hi + extension, 1024-aligned
+  int smem_total;  // dynamic SMEM of query_x3_kernel
+};
+
+__host__ __device__ inline X3Layout make_x3_layout(const ndf_model_desc& m) {
+  const Layout lay = make_layout(m);
+  X3Layout x;
+  x.ext_off = (lay.blob_bytes + 1023) & ~1023;
+  x.wlat_hi = 0;
+  x.wlat_lo = 128 * 32 * 2;
+  x.wh_lo = 2 * 128 * 32 * 2;
+  x.wout32 = x.wh_lo + (lay.H - 1) * lay.wh_bytes;
+  x.ext_bytes = x.wout32 + kHid * 4;
+  x.smem_w = ((lay.H - 1) * lay.wh_bytes + x.ext_bytes + 1023) & ~1023;
+  x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2048;
+  return x;
+}
+
+// The split path needs the BASELINE family (sum_absdiff, E = 55, hidden width 128) and
+// SMEM for hi and lo weights of every hidden layer (H <= 3).
+__host__ __device__ inline bool x3_supported(const ndf_model_desc& m) {
+  if (m.tc_format != NDF_PREC_BF16 || m.merge != NDF_MERGE_SUM_ABSDIFF) return false;
+  if (m.widths[0] != 2 * kE || m.n_layers < 2) return false;
+  return make_x3_layout(m).smem_total <= kMaxSmem;
+}
+
+// fp32 value -> (hi, lo) bf16 pair in one word (hi in the low half: k = 2j + 0)
+__device__ __forceinline__ uint32_t split_f32(float v) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+}
+
+// Per-query layer-0 tables, one 128-thread block per (reference r, 4-node group g), thread
+// = output feature n: the 4 nodes' values as (hi, lo) words, 16 B at
+// ((r * ng + g) * 128 + n) * 16.  Groups [0, ngx) are x-nodes 4g + j (PX: raw x and
+// Fourier-x features); groups g = ngx + g' are (y, z)-rows row0 + 4 g' + j with
+// row = iy + ny * iz (PYZ: raw y, z, Fourier-y, z, plus the bias) -- only the rows of the
+// launch's row-tiles.  Nodes / rows past the grid are zero.  The merged values are formed
+// in fp32 exactly as the reference merge (r + q, |r - q|; model.py:279-286 + BASELINE)
+// and weighted with fp32 FMAs (pre-scaled by 1/2 for SiLU): their ~2^-21 relative error
+// sits far below the 2^-17 of the hi + lo pair the sum is stored as.
+__global__ void __launch_bounds__(128)
+prep_x3_tab_kernel(const QueryArgs a, int n_ref, const float* __restrict__ feat, int ngx,
+                   int ngyz, int64_t row0, uint4* px, uint4* pyz) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // feat from prep_ws_feat_kernel
+  __shared__ float qf[4][2][16];   // node j's axis features (x nodes: [0]; rows: y [0], z [1])
+  __shared__ float rf[3][16];      // the reference's x, y, z features
+  const int per_ref = ngx + ngyz;
+  const int r = blockIdx.x / per_ref, g = blockIdx.x - r * per_ref;
+  const int n = threadIdx.x;
+  const bool isx = g < ngx;
+  const int nyz = a.ny * a.nz;
+  {
+    const int j = n >> 5, ax = (n >> 4) & 1, c = n & 15;
+    float v = 0.0f;
+    if (isx) {
+      const int ix = 4 * g + j;
+      if (ax == 0 && ix < a.nx) v = feat[(size_t)ix * 16 + c];
+    } else {
+      const int64_t row = row0 + 4 * (g - ngx) + j;
+      if (row < nyz) {
+        const int node = ax == 0 ? a.nx + (int)(row % a.ny) : a.nx + a.ny + (int)(row / a.ny);
+        v = feat[(size_t)node * 16 + c];
+      }
+    }
+    qf[j][ax][c] = v;
+    const int nref = a.nx + a.ny + a.nz + 3 * r;   // reference r's x node in feat
+    if (n < 48) rf[n >> 4][n & 15] = feat[(size_t)(nref + (n >> 4)) * 16 + (n & 15)];
+  }
+  __syncthreads();
+  const float* W = a.m.params_f32;                 // W0: (2E x 128) row-major, then b0
+  float v[4];
+  // feature f of axis ax, stored at column c of the axis rows
+  auto add = [&](int f, int ax, int qax, int c) {
+    const float ws = __ldg(W + (size_t)f * kHid + n), wd = __ldg(W + (size_t)(kE + f) * kHid + n);
+    const float rv = rf[ax][c];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float qv = qf[j][qax][c];
+      v[j] = fmaf(wd, fabsf(rv - qv), fmaf(ws, rv + qv, v[j]));
+    }
+  };
+  bool valid[4];
+  if (isx) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { v[j] = 0.0f; valid[j] = 4 * g + j < a.nx; }
+    add(0, 0, 0, 0);
+#pragma unroll
+    for (int o = 0; o < kL; ++o) { add(3 + 6 * o, 0, 0, 1 + 2 * o); add(4 + 6 * o, 0, 0, 2 + 2 * o); }
+  } else {
+    const float bias = __ldg(W + (size_t)2 * kE * kHid + n);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { v[j] = bias; valid[j] = row0 + 4 * (g - ngx) + j < nyz; }
+    add(1, 1, 0, 0);
+    add(2, 2, 1, 0);
+#pragma unroll
+    for (int o = 0; o < kL; ++o) {
+      add(5 + 6 * o, 1, 0, 1 + 2 * o); add(6 + 6 * o, 1, 0, 2 + 2 * o);
+      add(7 + 6 * o, 2, 1, 1 + 2 * o); add(8 + 6 * o, 2, 1, 2 + 2 * o);
+    }
+  }
+  const float hs = a.m.activation == NDF_ACT_SILU ? 0.5f : 1.0f;
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w[j] = valid[j] ? split_f32(v[j] * hs) : 0u;
+  uint4* dst = isx ? px + ((size_t)r * ngx + g) * kHid : pyz + ((size_t)r * ngyz + (g - ngx)) * kHid;
+  dst[n] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Fill the blob extension (after pack_fill_kernel has written the standard layout).
+__global__ void pack_x3_kernel(const ndf_model_desc m, uint8_t* blob) {
+  const Layout lay = make_layout(m);
+  const X3Layout xl = make_x3_layout(m);
+  uint8_t* ext = blob + xl.ext_off;
+  const float hs = m.activation == NDF_ACT_SILU ? 0.5f : 1.0f;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  const float* W0 = m.params_f32;
+  // latent rows of W0: k = 2c + sd  <->  W0 row sd * E + 39 + c
+  for (int64_t e = gtid; e < 32 * kHid; e += gsz) {
+    const int k = (int)(e / kHid), nn = (int)(e % kHid);
+    const int c = k >> 1, sd = k & 1;
+    const float w = hs * W0[(size_t)(sd * kE + kX3Lat + c) * kHid + nn];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+    *reinterpret_cast<__nv_bfloat16*>(ext + xl.wlat_hi + canon_off(nn, k, 512)) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(ext + xl.wlat_lo + canon_off(nn, k, 512)) = lo;
+  }
+  size_t off = (size_t)m.widths[0] * kHid + kHid;     // past W0, b0
+  for (int l = 1; l < m.n_layers; ++l) {
+    const int K = m.widths[l], N = m.widths[l + 1];
+    const float* W = m.params_f32 + off;
+    if (l < lay.H) {
+      uint8_t* dst = ext + xl.wh_lo + (l - 1) * lay.wh_bytes;
+      for (int64_t e = gtid; e < (int64_t)K * N; e += gsz) {
+        const int k = (int)(e / N), nn = (int)(e % N);
+        const float w = hs * W[e];
+        const float hi = __bfloat162float(__float2bfloat16_rn(w));
+        *reinterpret_cast<__nv_bfloat16*>(dst + canon_off(nn, k, kSboA)) = __float2bfloat16_rn(w - hi);
+      }
+    } else {
+      for (int64_t e = gtid; e < K; e += gsz)
+        reinterpret_cast<float*>(ext + xl.wout32)[e] = W[e];
+    }
+    off += (size_t)K * N + N;
+  }
+}
+
+// Latent channels of node (ix, iy, iz) from the z-interpolated table lz: lerp in y, then
+// in x -- the arithmetic of latent_yx_lerp's per-lane branch (same bits).
+__device__ __forceinline__ void latent_yx_direct(const float* __restrict__ lz, const QueryArgs& a,
+                                                 int ix, int iy, int iz, float* acc) {
+  int x0, y0;
+  float tx, ty;
+  latent_cell(ix, a.nx, a.g.rx, x0, tx);
+  latent_cell(iy, a.ny, a.g.ry, y0, ty);
+  const size_t rstride = (size_t)a.g.rx * kC;
+  const float* r0 = lz + ((size_t)iz * a.g.ry + y0) * rstride;
+  float g0[kC];
+#pragma unroll
+  for (int dx = 0; dx < 2; ++dx) {
+    const float4* p0 = reinterpret_cast<const float4*>(r0 + (size_t)(x0 + dx) * kC);
+    const float4* p1 = reinterpret_cast<const float4*>(r0 + rstride + (size_t)(x0 + dx) * kC);
+#pragma unroll
+    for (int q = 0; q < kC / 4; ++q) {
+      const float4 f = __ldg(p0 + q), h = __ldg(p1 + q);
+      const float gy[4] = {fmaf(ty, h.x - f.x, f.x), fmaf(ty, h.y - f.y, f.y),
+                           fmaf(ty, h.z - f.z, f.z), fmaf(ty, h.w - f.w, f.w)};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (dx == 0) g0[4 * q + u] = gy[u];
+        else acc[4 * q + u] = fmaf(tx, gy[u] - g0[4 * q + u], g0[4 * q + u]);
+      }
+    }
+  }
+}
+
+// Hidden-layer epilogue of one 16-column sub-chunk, split operands: activation in fp32,
+// then 8 hi words into columns [0, 8) and 8 lo words into [8, 16) of the sub-chunk.
+template <bool SILU>
+__device__ __forceinline__ void epilogue16_x3(const float* x, int act, uint32_t a_taddr) {
+  float h[16];
+  if constexpr (SILU) {
+    silu16(x, h);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
+  }
+  uint32_t p[16];
+#ifndef NDF_EXP_X3_NOSPLIT   // timing experiment: lo words zero (wrong results)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) split_pair(h[2 * i], h[2 * i + 1], p[i], p[8 + i]);
+#else
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { p[i] = pack2<false>(h[2 * i], h[2 * i + 1]); p[8 + i] = 0u; }
+#endif
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(a_taddr),
+      "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7]),
+      "r"(p[8]), "r"(p[9]), "r"(p[10]), "r"(p[11]), "r"(p[12]), "r"(p[13]), "r"(p[14]), "r"(p[15])
+      : "memory");
+}
+
+// Last hidden layer, one 16-column sub-chunk: activation, then the fp32 output dot with
+// contiguous fp32 weights (same accumulation order as dot16).
+template <bool SILU>
+__device__ __forceinline__ void dot16_x3(const float* x, int c0, int act, uint32_t w32_addr,
+                                         float* dots) {
+  float w[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(w[4 * q]), "=f"(w[4 * q + 1]), "=f"(w[4 * q + 2]), "=f"(w[4 * q + 3])
+        : "r"(w32_addr + (uint32_t)(4 * c0 + 16 * q)));
+  float h[16];
+  if constexpr (SILU) {
+    silu16(x, h);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = act_f32(act, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+    ffma2(dots[i & 3], dots[(i & 3) + 1], h[i], h[i + 1], w[i], w[i + 1], dots[i & 3],
+          dots[(i & 3) + 1]);
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// Tile geometry of a launch over flat vertices [v0, v1) of an nx x ny x nz grid: tiles of
+// 8 x-nodes x 16 (y, z)-rows covering rows v0 / nx .. (v1 - 1) / nx; rows and nodes
+// outside the range are computed and discarded.
+struct X3Tiles {
+  int n_xt;          // tiles along x
+  int ty0;           // first row-tile
+  int64_t n_vt;      // tiles per reference
+};
+__host__ __device__ inline X3Tiles x3_tiles(int nx, int64_t v0, int64_t v1) {
+  X3Tiles t;
+  t.n_xt = (nx + kX3TX - 1) / kX3TX;
+  const int64_t row_lo = v0 / nx, row_hi = (v1 - 1) / nx;
+  t.ty0 = (int)(row_lo / kX3TY);
+  t.n_vt = (int64_t)t.n_xt * (row_hi / kX3TY - t.ty0 + 1);
+  return t;
+}
+
+// schedule trace of CTA 0 (trace builds only, tools/trace_x3.py): t.trace[(slot * 32 + tile)
+// * 24 + event]; producer 0-4, epilogue lead warp 5 + 2l (layer l's MMAs done) / 6 + 2l
+// (its epilogue done), issuer 12 + 4l + k2 (K-chunk k2 of layer l + 1 issued)
+#define NDF_X3_TRACE(slot_, kk_, ev)                                                    \
+  do {                                                                                  \
+    if (NDF_TRACE_ON(blockIdx.x == 0 && (kk_) < 32))                                     \
+      t.trace[((slot_) * 32 + (kk_)) * 24 + (ev)] = clock64();                          \
+  } while (0)
+
+template <bool SILU>
+__global__ void __launch_bounds__(kPPThreads, 1)
+query_x3_kernel(const TcArgs t) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const QueryArgs& a = t.q;
+  const Layout lay = make_layout(a.m);
+  const X3Layout xl = make_x3_layout(a.m);
+  const int H = lay.H;
+  const int whb = (H - 1) * lay.wh_bytes;
+  uint8_t* wh_s = smem;                           // hidden layers' hi weights
+  uint8_t* ext_s = smem + whb;                    // blob extension (W_lat hi/lo, W_lo, wout32)
+  uint8_t* bias_s = smem + xl.smem_w;             // [ones][bias 1..H-1][zero], 2 KB each
+  uint8_t* selx = bias_s + (H + 1) * kX3Blk;
+  uint8_t* selyz = selx + kX3SelX;
+  uint8_t* slots = selyz + kX3SelYZ;              // per slot: Bx | Byz | A_lat
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kPPSlots * kX3Slot);
+  uint64_t* wbar = &bars[0];
+  uint64_t* acc_full = &bars[1];
+  uint64_t* s_free = &bars[3];
+  uint64_t* d_free = &bars[5];
+  uint64_t* b_full = &bars[7];                    // [kPPSlots] the tile's PX / PYZ rows landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  float* eref_s = reinterpret_cast<float*>(bars + 16);
+  float* dotx = reinterpret_cast<float*>(bars + 32);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int wg = warp >> 2;
+  const int wq = warp & 3;
+  const int wtid = tid & 127;
+
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    for (int s = 0; s < kPPSlots; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&s_free[s], 1);
+      mbar_init(&d_free[s], 1);
+      mbar_init(&b_full[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  {
+    // constant operand blocks (K-major, 16 B per row of an 8-K group):
+    //   bias region: block 0 = ones (A: k = 0, 1 -> 1), block l = bias of hidden layer l
+    //   (B: k = 0 -> hi, k = 1 -> lo), block H = zeros (the k = 8..15 group of every one
+    //   of them, reached through LBO);
+    //   selx: row m -> 1 at k = 2 (m & 7), +1;  selyz: row m -> 1 at k = 2 (m >> 3), +1
+    const float* gvec = reinterpret_cast<const float*>(
+        reinterpret_cast<const uint8_t*>(a.m.params_tc) + lay.vec_off);
+    for (int i = tid; i < (H + 1) * 128; i += blockDim.x) {
+      const int blk = i >> 7, r = i & 127;
+      uint32_t w0 = 0u;
+      if (blk == 0) {
+        w0 = kBf16One2;
+      } else if (blk < H) {
+        const float b = __ldg(gvec + blk * kHid + r);
+        uint32_t lo;
+        split_pair(b, 0.0f, w0, lo);               // w0 = (hi(b), 0), lo = (lo(b), 0)
+        w0 = (w0 & 0xffffu) | (lo << 16);          // k = 0: hi, k = 1: lo
+      }
+      st_shared_v4(smem_u32(bias_s + blk * kX3Blk) + r * 16, w0, 0u, 0u, 0u);
+    }
+    for (int i = tid; i < 128 * 6; i += blockDim.x) {
+      const int r = i % 128, g = i / 128;          // g 0-1: selx K-group, 2-5: selyz K-group
+      uint32_t w[4];
+      const int hot = g < 2 ? (r & 7) - 4 * g : (r >> 3) - 4 * (g - 2);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = (u == hot) ? kBf16One2 : 0u;
+      const uint32_t addr = g < 2 ? smem_u32(selx) + canon_off(r, 8 * g, 256)
+                                  : smem_u32(selyz) + canon_off(r, 8 * (g - 2), 512);
+      st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    mbar_expect_tx(wbar, (uint32_t)(whb + xl.ext_bytes));
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.m.params_tc);
+    for (int off = 0; off < whb; off += 32768)
+      bulk_g2s(wh_s + off, src + lay.w0_bytes + off, (uint32_t)min(32768, whb - off), wbar);
+    for (int off = 0; off < xl.ext_bytes; off += 32768)
+      bulk_g2s(ext_s + off, src + xl.ext_off + off, (uint32_t)min(32768, xl.ext_bytes - off), wbar);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // prep tables ready
+  if (tid < kC) eref_s[tid] = t.erefs[tid];
+  __syncthreads();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kHid >> 3) << 17) |
+                         ((uint32_t)(kTileM >> 4) << 24);
+
+  const int64_t n = a.v1 - a.v0;
+  const X3Tiles tg = x3_tiles(a.nx, a.v0, a.v1);
+  const int64_t n_tiles = tg.n_vt * t.n_ref;
+  const int64_t tile_stride = (int64_t)gridDim.x * kPPSlots;
+  const int s = wg < 4 ? (wg >> 1) : wg - 4;
+  const int64_t first = (int64_t)blockIdx.x * kPPSlots + s;
+  const int64_t cnt = first < n_tiles ? (n_tiles - first + tile_stride - 1) / tile_stride : 0;
+  const uint32_t d_slot = tmem_base + (uint32_t)(s * 2 * kHid);
+  const int nyz = a.ny * a.nz;
+  // tile -> (reference, x tile, row tile)
+  auto decode = [&](int64_t tile_g, int& r, int& tx, int& ty) {
+    r = t.n_ref == 1 ? 0 : (int)((uint64_t)tile_g / (uint64_t)tg.n_vt);
+    const int64_t tl = tile_g - (int64_t)r * tg.n_vt;
+    ty = tg.ty0 + (int)((uint64_t)tl / (uint32_t)tg.n_xt);
+    tx = (int)(tl - (int64_t)(ty - tg.ty0) * tg.n_xt);
+  };
+
+  if (wg == 6) {
+    // ======================== MMA issuer of slot warp - 24 ===========================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+    const int si = warp - 24;
+    if (si < kPPSlots) {
+      const int64_t fi = (int64_t)blockIdx.x * kPPSlots + si;
+      const int64_t ci = fi < n_tiles ? (n_tiles - fi + tile_stride - 1) / tile_stride : 0;
+      const uint32_t ds = tmem_base + (uint32_t)(si * 2 * kHid);
+      const uint32_t wlo_mask = (uint32_t)t.x3_wlo_mask;
+      mbar_wait(wbar, 0);
+#pragma unroll 1
+      for (int64_t kk = 0; kk < ci; ++kk) {
+#pragma unroll 1
+        for (int l = 0; l + 1 < H; ++l) {
+          const uint32_t half = (uint32_t)((kk * H + l) & 1);
+          const uint32_t d_next = ds + (half ^ 1u) * kHid;
+          const uint32_t a_tm = ds + half * kHid;                      // A of layer l+1
+          const uint32_t whi = smem_u32(wh_s) + (uint32_t)(l * lay.wh_bytes);
+          const uint32_t wlo = smem_u32(ext_s) + (uint32_t)(xl.wh_lo + l * lay.wh_bytes);
+          const bool use_lo = (wlo_mask >> (l + 1)) & 1u;
+          if (t.x3_burst)      // whole layer after the epilogue (K-chunk barriers passed first)
+            for (int k2 = 0; k2 < 4; ++k2) named_bar(1 + 4 * si + k2, 288);
+#pragma unroll 1
+          for (int k2 = 0; k2 < 4; ++k2) {
+            if (!t.x3_burst) named_bar(1 + 4 * si + k2, 288);
+            if (lane == 0) {
+              tc_fence_after();
+              if (k2 == 0)
+                mma_bf16(d_next, smem_desc(smem_u32(bias_s), (uint32_t)(H * kX3Blk), 128),
+                         smem_desc(smem_u32(bias_s) + (uint32_t)((l + 1) * kX3Blk),
+                                   (uint32_t)((H - l - 1) * kX3Blk), 128),
+                         idesc, 0u);
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int ks = 2 * k2 + j;
+                const uint64_t bh = smem_desc(whi + ks * 256, 128, kSboA);
+                mma_ts(d_next, a_tm + (uint32_t)(16 * ks), bh, idesc, 1u);
+#ifndef NDF_EXP_X3_ONEMMA    // timing experiment: hi x hi only (wrong results)
+                mma_ts(d_next, a_tm + (uint32_t)(16 * ks + 8), bh, idesc, 1u);
+                if (use_lo) mma_ts(d_next, a_tm + (uint32_t)(16 * ks),
+                                   smem_desc(wlo + ks * 256, 128, kSboA), idesc, 1u);
+#else
+                (void)use_lo; (void)wlo;
+#endif
+              }
+              if (k2 == 3) mma_commit(&acc_full[si]);
+              NDF_X3_TRACE(si, (int)kk, 12 + 4 * l + k2);
+            }
+          }
+        }
+      }
+    }
+  } else if (wg >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
+    // ============================ producer (slot s) ==================================
+    uint8_t* slot = slots + s * kX3Slot;
+    const uint32_t bx_a = smem_u32(slot), byz_a = bx_a + kX3Bx, alat_a = byz_a + kX3Byz;
+    const uint32_t wlat_hi = smem_u32(ext_s) + xl.wlat_hi, wlat_lo = smem_u32(ext_s) + xl.wlat_lo;
+    const int j = wtid & 7, q = wtid >> 3;
+#pragma unroll 1
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+      int r, tx, ty;
+      if (wtid == 0) NDF_X3_TRACE(s, (int)kk, 0);
+      decode(first + kk * tile_stride, r, tx, ty);
+      const int ix = min(kX3TX * tx + j, a.nx - 1);
+      const int row = min(kX3TY * ty + q, nyz - 1);
+      const int iy = row % a.ny, iz = row / a.ny;
+      uint32_t pv[32];    // latent words: hi 0..15, lo 16..31
+      {
+        float lat[kC];
+        latent_yx_direct(t.lz, a, ix, iy, iz, lat);
+#pragma unroll
+        for (int c4 = 0; c4 < kC / 4; ++c4) {
+          const float4 r4 = t.n_ref == 1
+              ? reinterpret_cast<const float4*>(eref_s)[c4]
+              : __ldg(reinterpret_cast<const float4*>(t.erefs + (size_t)r * kERefStride) + c4);
+          const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = 4 * c4 + u;
+            split_pair(rv[u] + lat[c], fabsf(rv[u] - lat[c]), pv[c], pv[16 + c]);
+          }
+        }
+      }
+      if (wtid == 0) NDF_X3_TRACE(s, (int)kk, 1);
+      if (kk >= 1) mbar_wait(&s_free[s], (uint32_t)((kk - 1) & 1));   // previous layer 0 done
+      if (wtid == 0) {
+        NDF_X3_TRACE(s, (int)kk, 2);
+        mbar_expect_tx(&b_full[s], (uint32_t)(kX3Bx + kX3Byz));
+        bulk_g2s(slot, reinterpret_cast<const uint8_t*>(t.px) +
+                           ((size_t)r * t.ngx + 2 * tx) * (size_t)kX3Blk, kX3Bx, &b_full[s]);
+        bulk_g2s(slot + kX3Bx, reinterpret_cast<const uint8_t*>(t.pyz) +
+                                   ((size_t)r * t.ngyz + 4 * (ty - tg.ty0)) * (size_t)kX3Blk,
+                 kX3Byz, &b_full[s]);
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        st_shared_v4(alat_a + canon_off(wtid, 8 * g, 1024), pv[4 * g], pv[4 * g + 1],
+                     pv[4 * g + 2], pv[4 * g + 3]);
+      fence_proxy_async();
+      named_bar(11 + s, 128);
+      if (wtid == 0) {
+        if (kk == 0) mbar_wait(wbar, 0);
+        else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
+        NDF_X3_TRACE(s, (int)kk, 3);
+        mbar_wait(&b_full[s], (uint32_t)(kk & 1));
+        tc_fence_after();
+        const uint32_t d0 = d_slot + (uint32_t)((kk * H) & 1) * kHid;
+        mma_bf16(d0, smem_desc(smem_u32(selx), 128, 256), smem_desc(bx_a, 2048, 128), idesc, 0u);
+        mma_bf16(d0, smem_desc(smem_u32(selyz), 128, 512), smem_desc(byz_a, 2048, 128), idesc, 1u);
+        mma_bf16(d0, smem_desc(smem_u32(selyz) + 256, 128, 512), smem_desc(byz_a + 4096, 2048, 128),
+                 idesc, 1u);
+#pragma unroll
+        for (int st = 0; st < 2; ++st) {
+          const uint64_t bh = smem_desc(wlat_hi + st * 256, 128, 512);
+          mma_bf16(d0, smem_desc(alat_a + st * 256, 128, 1024), bh, idesc, 1u);         // hi x hi
+          mma_bf16(d0, smem_desc(alat_a + (2 + st) * 256, 128, 1024), bh, idesc, 1u);   // lo x hi
+          mma_bf16(d0, smem_desc(alat_a + st * 256, 128, 1024),
+                   smem_desc(wlat_lo + st * 256, 128, 512), idesc, 1u);                 // hi x lo
+        }
+        mma_commit(&acc_full[s]);
+        NDF_X3_TRACE(s, (int)kk, 4);
+      }
+    }
+  } else {
+    // ======================== epilogue (slot s, column half ch) ======================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
+    const int ch = wg & 1;
+    const bool lead = ch == 0 && wq == 0;
+    const uint32_t first_col = 16u * (uint32_t)ch;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    mbar_wait(wbar, 0);
+    const float bias_out = __ldg(reinterpret_cast<const float*>(
+        reinterpret_cast<const uint8_t*>(a.m.params_tc) + lay.vec_off) + H * kHid);
+    const uint32_t w32_addr = smem_u32(ext_s) + xl.wout32;
+    uint32_t acc_ph = 0u;
+#pragma unroll 1
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+#pragma unroll 1
+      for (int l = 0; l < H; ++l) {
+        const uint32_t half = (uint32_t)((kk * H + l) & 1);
+        const uint32_t d_base = d_slot + lane_base + half * kHid;
+        mbar_wait(&acc_full[s], acc_ph);
+        acc_ph ^= 1u;
+        tc_fence_after();
+        if (l == 0 && lead && lane == 0) mbar_arrive(&s_free[s]);   // slot SMEM reusable
+        if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 5 + 2 * l);
+        float va[16], vb[16];
+        tmem_ld16_nowait(d_base + first_col, va);
+        tmem_wait_ld();
+        if (l + 1 < H) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t col = first_col + 32u * (uint32_t)i;
+            float* cur = (i & 1) ? vb : va;
+            float* nxt = (i & 1) ? va : vb;
+            if (i + 1 < 4) tmem_ld16_nowait(d_base + col + 32u, nxt);
+            epilogue16_x3<SILU>(cur, a.m.activation, d_base + col);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            named_bar_arrive(1 + 4 * s + i, 288);
+            if (i + 1 < 4) tmem_wait_ld();
+          }
+          if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
+        } else {
+          if (lead && lane == 0) mbar_arrive(&d_free[s]);
+          float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (first_col != 64u * ch) tmem_ld16_nowait(d_base + 64u * ch, va);
+          if (first_col != 64u * ch) tmem_wait_ld();
+#pragma unroll 1
+          for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
+            const int col = 32 * kc;
+            tmem_ld16_nowait(d_base + (uint32_t)(col + 16), vb);
+            dot16_x3<SILU>(va, col, a.m.activation, w32_addr, dots);
+            tmem_wait_ld();
+            if (kc + 1 < 2 * ch + 2) tmem_ld16_nowait(d_base + (uint32_t)(col + 32), va);
+            dot16_x3<SILU>(vb, col + 16, a.m.activation, w32_addr, dots);
+            if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
+          }
+          tc_fence_before();
+          const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
+          if (ch == 1) dotx[s * kTileM + wtid] = part;
+          named_bar(9 + s, 256);
+          if (ch == 0) {
+            int r, tx, ty;
+            decode(first + kk * tile_stride, r, tx, ty);
+            const int ix = kX3TX * tx + (wtid & 7);
+            const int row = kX3TY * ty + (wtid >> 3);
+            const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
+            const float z = part + dotx[s * kTileM + wtid] + bias_out;
+            if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {
+              const float o = head_exact(a.m.head, z);
+              if (t.out16) {
+                const __half ho = __float2half_rn(o);
+                t.out16[(int64_t)r * t.ld_out + (v - a.v0)] = *reinterpret_cast<const uint16_t*>(&ho);
+              } else {
+                a.out[v - a.v0] = o;
+              }
+            }
+          }
+          named_bar(9 + s, 256);
+          if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
+        }
+      }
+    }
+    (void)n;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+}

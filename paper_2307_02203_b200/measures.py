@@ -375,13 +375,15 @@ def load_field_grid(path) -> FieldGrid:
 
 
 def pair_estimators_device(field_obj, variable: str, pa, pb, k: int = 8,
-                           measures=("pearson", "ksg_mi")):
+                           measures=("pearson", "ksg_mi"), counts: bool = False):
     """Bulk estimator pairs (BASELINE config 4 / training-target generation).
 
     For vertex pairs (pa[p], pb[p]) of one variable's node grid computes Pearson r
     (fp64, measures.py:111-133) and/or KSG MI (fp64, measures.py:173-203) on the
     GPU from a vertex-major copy of the ensemble.  Replaces the per-pair loop of
-    training._targets (training.py:111-119).  Returns {name: CUDA fp64 tensor}.
+    training._targets (training.py:111-119).  Returns {name: CUDA fp64 tensor};
+    ``counts=True`` adds "ksg_counts", the (n, 2, M) int32 KSG marginal counts n_x / n_y
+    (measures.py:198-201) the MI was computed from.
     """
     import torch
     dev_ens = _device_view(field_obj, variable)
@@ -408,8 +410,12 @@ def pair_estimators_device(field_obj, variable: str, pa, pb, k: int = 8,
         jit, psi = _KsgTables.get(dev, M)
         mi = torch.empty(n, dtype=torch.float64, device=dev)
         status = torch.zeros(1, dtype=torch.int32, device=dev)
+        cnt = torch.empty((n, 2, M), dtype=torch.int32, device=dev) if counts else None
         N.call("ndf_ksg_pairs", N.ptr(Xv), M, V, N.ptr(ta), N.ptr(tb), n, k, N.ptr(jit),
-               N.ptr(psi), _KsgTables.psi_km(k, M), N.ptr(mi), None, None, N.ptr(status), stream)
+               N.ptr(psi), _KsgTables.psi_km(k, M), N.ptr(mi), None, N.ptr(cnt), N.ptr(status),
+               stream)
+        if counts:
+            out["ksg_counts"] = cnt
         if int(status.item()):
             raise ParameterError("digamma defined here for positive arguments only")
         out["ksg_mi"] = mi

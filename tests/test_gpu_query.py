@@ -19,11 +19,15 @@ from paper_2307_02203_b200 import workloads as W  # noqa: E402
 
 TOL32 = 1e-5
 TOL16 = 1e-2          # north_star: 16-bit tensor-core MLP vs the fp32 reference output
-# Plain bf16 operands carry 8 significant bits: on the O(1)-latent parity model the
-# pure quantisation error (reproduced bit-for-bit by a NumPy bf16 simulation, see
-# DESIGN.md) reaches ~1.2e-2 at c0, so bf16 is held to 2e-2 and fp16 operands
-# (same tcgen05 kind::f16 path, 11 significant bits) to the 1e-2 contract.
-TOL_BF16 = 2e-2
+# bf16 runs split operands (hi + lo bf16 pairs: query_x3_kernel for grid queries of the
+# BASELINE family, a hi/lo A plane on the classic kernel otherwise), so it is held to the
+# north_star's 1e-2 like fp16; plain bf16 operands would reach ~1.4e-2 at config-1 scale
+# (tools/bf16_sim.py).
+TOL_BF16 = 1e-2
+# The classic schedule (paired forward, the reference's other merges) splits only the
+# activations: its bf16 weights keep their 2^-9 rounding, which on the reference
+# family's SnakeAlt / linear-head models measures ~1.0e-2 relative to the output scale.
+TOL_BF16_CLASSIC = 1.5e-2
 
 
 def refmode_model(g, merge, precision):
@@ -65,10 +69,10 @@ def test_reference_mode_golden_16bit(golden, merge):
         got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
         want = g[f"{merge}_out{r}"]
         # linear head, unbounded output: tolerance relative to the output scale
-        assert np.max(np.abs(got - want)) <= TOL_BF16 * max(1.0, np.abs(want).max())
+        assert np.max(np.abs(got - want)) <= TOL_BF16_CLASSIC * max(1.0, np.abs(want).max())
     got = model.forward(g[f"{merge}_p1"], g[f"{merge}_p2"])
     want = g[f"{merge}_fwd"]
-    assert np.max(np.abs(got - want)) <= TOL_BF16 * max(1.0, np.abs(want).max())
+    assert np.max(np.abs(got - want)) <= TOL_BF16_CLASSIC * max(1.0, np.abs(want).max())
     model = refmode_model(g, merge, "fp16")
     for r, ref in enumerate(g["refs"]):
         got = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, dims).values
@@ -121,15 +125,19 @@ def test_c0_other_activations_16bit(c0, act):
     p1, p2 = rng.uniform(-1, 1, (500, 3)), rng.uniform(-1, 1, (500, 3))
     want_pts = om.forward(p1, p2)
     assert np.max(np.abs(ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims).values - want)) <= TOL32
-    # bf16: operand rounding alone (tools/bf16_sim.py <act>, same model family) gives
-    # 1.3e-2 (relu), 2.9e-2 (snake_alt) and 8.2e-2 (snake: derivative up to 2, unbounded)
-    # -- bounded here at 1.5x that; fp16 stays inside the 1e-2 contract for all three
-    tol_bf16 = {"relu": 2e-2, "snake_alt": 4.5e-2, "snake": 0.125}[act]
-    for prec, tol in (("fp16", TOL16), ("bf16", tol_bf16)):
+    # grid queries: fp16 and split bf16 (query_x3_kernel) inside the 1e-2 contract.
+    # Paired forward on the classic schedule with bf16 keeps the weights' bf16 rounding:
+    # measured 6.6e-3 (relu), 1.7e-2 (snake_alt) and 3.1e-2 (snake: derivative up to 2,
+    # unbounded) -- bounded at ~1.5x that.
+    tol_pts_bf16 = {"relu": 1e-2, "snake_alt": 2.5e-2, "snake": 4.5e-2}[act]
+    for prec, tol_pts in (("fp16", TOL16), ("bf16", tol_pts_bf16)):
         m = model.with_precision(prec)
         got = ndf.reconstruct_field(m, ref, ndf.ROLE_MU, w.dims).values
-        assert np.max(np.abs(got - want)) <= tol, (act, prec)
-        assert np.max(np.abs(m.forward(p1, p2) - want_pts)) <= tol, (act, prec)
+        eg = np.max(np.abs(got - want))
+        ep = np.max(np.abs(m.forward(p1, p2) - want_pts))
+        print(f"{act} {prec}: grid {eg:.3e} points {ep:.3e}")
+        assert eg <= (TOL16 if prec == "fp16" else TOL_BF16), (act, prec)
+        assert ep <= tol_pts, (act, prec)
 
 
 def test_c0_concat_merge_16bit(c0):
@@ -169,6 +177,11 @@ def test_decoder_depth_envelope(layers):
     ref, dims = (0.2, -0.3, 0.5), (21, 13, 5)
     want = O.reconstruct_field(om, ref, dims)
     for prec, tol in (("fp16", TOL16), ("bf16", TOL_BF16)):
+        if prec == "bf16" and layers == 6:
+            # 5 hidden layers: the resident weights leave no room for the hi and lo A planes
+            with pytest.raises(ndf.ConfigError):
+                model.with_precision(prec).forward(np.zeros((1, 3)), np.zeros((1, 3)))
+            continue
         got = ndf.reconstruct_field(model.with_precision(prec), ref, ndf.ROLE_MU, dims).values
         assert np.max(np.abs(got - want)) <= tol, (layers, prec)
     deep = ndf.NdfModel.build(ndf.ModelSpec(grid_resolution=(4, 6, 2), decoder_layers=9,
@@ -225,7 +238,8 @@ def test_batch_invariance_and_vertex_ranges(c0):
             # the output layer as an fp32 dot product; the points kernel takes fp64
             # positions and a 16-bit output MMA -> both sit within their precision of
             # the fp32 oracle, not bitwise on each other
-            tol = 4e-3 if prec == "fp16" else 1.5e-2
+            tol = 4e-3
+            print(f"{prec} points vs grid {np.max(np.abs(looped - full[:50])):.3e}")
             assert np.max(np.abs(looped - full[:50])) <= tol
 
 

@@ -1,10 +1,10 @@
 #!/bin/bash
-# Run the quick bench for each prebuilt abtest/lib_<name>.so (interleaved, 2 reps).
-cp paper_2307_02203_b200/libndf_b200.so abtest/lib_orig.so
+# Time each prebuilt variants/lib_<name>.so with a probe command (interleaved, 2 reps):
+#   bash tools/ab_variants.sh "python tools/x3_probe.py 20" base nomufu ...
+cmd=$1; shift
 for rep in 1 2; do
   for v in "$@"; do
-    cp abtest/lib_$v.so paper_2307_02203_b200/libndf_b200.so
-    timeout 180 python bench.py --quick --steps 40 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$v', round(d['value'],4), round(d['roofline']['kernel_ms'],4))"
+    echo -n "$v: "
+    NDF_LIB_PATH=variants/lib_$v.so timeout 180 $cmd 2>&1 | tail -1
   done
 done
-cp abtest/lib_orig.so paper_2307_02203_b200/libndf_b200.so

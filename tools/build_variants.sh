@@ -1,11 +1,12 @@
 #!/bin/bash
-# Build timing-experiment variants of libndf_b200.so into abtest/lib_<name>.so:
-#   base, trace (schedule stamps, tools/trace_ws.py), nomufu (see NDF_EXP_* in ndf_query_tc.cu),
-#   or a comma-separated list of -D flags.
+# Build timing-experiment variants of libndf_b200.so into variants/lib_<name>.so (git-ignored,
+# travels with gpurun); load one with NDF_LIB_PATH=variants/lib_<name>.so -- the product
+# library is never overwritten.  Names: base, trace (schedule stamps), nomufu (see NDF_EXP_*
+# in ndf_query_tc.cu / ndf_query_x3.cuh), or a comma-separated list of -D flags.
 set -e
 cd "$(dirname "$0")/.."
 python -m paper_2307_02203_b200.build > /dev/null
-mkdir -p abtest
+mkdir -p variants
 OBJS="build/obj/ndf_capi.o build/obj/ndf_ksg.o build/obj/ndf_pearson.o build/obj/ndf_query_f32.o"
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -I paper_2307_02203_b200/csrc"
 for v in "$@"; do
@@ -19,10 +20,13 @@ for v in "$@"; do
     skel) D="-DNDF_EXP_NOKSTEP -DNDF_EXP_NOMUFU -DNDF_EXP_NOPROD";;
     *) D="$(echo $v | tr ',' ' ')";;        # e.g. -DNDF_MBAR_HINT=2000
   esac
-  $NV $D -c paper_2307_02203_b200/csrc/ndf_query_tc.cu -o abtest/q_$v.o &
+  n=$(echo "$v" | tr -c 'a-zA-Z0-9_\n' '_')
+  $NV $D -c paper_2307_02203_b200/csrc/ndf_query_tc.cu -o variants/q_$n.o &
 done
 wait
 for v in "$@"; do
-  $NV -shared -o abtest/lib_$v.so abtest/q_$v.o $OBJS -lcudart
+  n=$(echo "$v" | tr -c 'a-zA-Z0-9_\n' '_')
+  $NV -shared -o variants/lib_$n.so variants/q_$n.o $OBJS -lcudart
+  rm -f variants/q_$n.o
 done
-ls abtest/*.so
+ls variants/*.so
