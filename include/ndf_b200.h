@@ -122,6 +122,18 @@ int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int64_t n_mu,
                      const double* p_nu, int64_t n, int32_t precision, float* out,
                      void* stream);
 
+/* Positional encoder alone: NdfModel.embed (model.py:169-177) -- [raw xyz |
+ * Fourier(L) | latent] computed in fp64 and cast to fp32, bit-identical to the
+ * reference.  branch 0 = the mu grid, 1 = the nu grid.  out is (n, E) fp32 row-major,
+ * E = 3 + 6L + max(levels, 1) * C (device or pinned host memory).  The query kernels
+ * fuse this step; these entry points serve callers that need the embedding itself.
+ * ndf_embed_nodes: grid nodes [v0, v1) of nx x ny x nz (x fastest, measures.py:240-252).
+ * ndf_embed_points: fp64 positions pos (n, 3), device memory. */
+int ndf_embed_nodes(const ndf_model_desc* m, int32_t branch, int32_t nx, int32_t ny, int32_t nz,
+                    int64_t v0, int64_t v1, float* out, void* stream);
+int ndf_embed_points(const ndf_model_desc* m, int32_t branch, const double* pos, int64_t n,
+                     float* out, void* stream);
+
 /* Batched multi-reference query (BASELINE config 3; the loop in
  * service.matrix_reconstruct, service.py:97-125, batched): refs is (n_ref, 3)
  * fp64 device; out is fp16 (n_ref rows of ld_out halfs), row r holds

@@ -18,8 +18,8 @@ from .measures import (CorrelationMeasure, FieldGrid, digamma, gaussian_mi_analy
                        grid_positions, ground_truth_field, ground_truth_field_device, ksg_mi,
                        ksg_rows, load_field_grid, pair_estimators_device, pearson,
                        pearson_against, pearson_rowwise, save_field_grid)
-from .model import DeviceModel, ModelSpec, NdfModel, load_model, save_model
-from .service import (ROLE_MU, ROLE_NU, benchmark, difference_field, matrix_reconstruct,
+from .model import DeviceModel, ModelSpec, NdfModel, as_model, load_model, save_model
+from .service import (ROLE_MU, ROLE_NU, benchmark, difference_field, forward, matrix_reconstruct,
                       reconstruct_field, reconstruct_field_device, reconstruct_multi_device)
 
 __version__ = "0.1.0"
@@ -29,7 +29,7 @@ __all__ = [
     "DeviceEnsemble", "DeviceError", "DeviceModel", "EnsembleField", "FieldGrid", "FormatError",
     "GridDomain", "ModelCorruptError", "ModelSpec", "NdfError", "NdfModel", "NotFoundError",
     "ParameterError", "ROLE_MU", "ROLE_NU", "ShapeError", "TrainingError", "UnknownVariableError",
-    "benchmark", "difference_field", "digamma", "gaussian_mi_analytic", "grid_positions",
+    "as_model", "benchmark", "difference_field", "forward", "digamma", "gaussian_mi_analytic", "grid_positions",
     "ground_truth_field", "ground_truth_field_device", "ksg_mi", "ksg_rows", "load_ensemble",
     "load_ensemble_device",
     "load_field_grid", "load_model", "matrix_reconstruct", "pair_estimators_device", "pearson",

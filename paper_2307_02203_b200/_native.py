@@ -74,6 +74,9 @@ SIGNATURES = {
                                       _i32, _i32, _i64, _i64, _i32, _c_p, _c_p]),
     "ndf_query_points": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _c_p, _i64, _c_p, _i64, _i32,
                                         _c_p, _c_p]),
+    "ndf_embed_nodes": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _i32, _i32, _i32, _i32, _i64,
+                                       _i64, _c_p, _c_p]),
+    "ndf_embed_points": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _i32, _c_p, _i64, _c_p, _c_p]),
     "ndf_query_grid_multi": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _c_p, _i32, _i32, _i32,
                                             _i32, _i32, _i64, _i64, _c_p, _i64, _c_p]),
     "ndf_sample_many": (ctypes.c_int, [_c_p, _i32, _i32, _i32, _i32, _c_p, _i64, _c_p, _c_p]),

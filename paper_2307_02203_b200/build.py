@@ -9,6 +9,7 @@ snapshot to the GPU box (it is git-ignored, not gpurun-ignored).
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
 import shutil
 import subprocess
@@ -36,12 +37,29 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
+def _sha(*parts) -> str:
+    h = hashlib.sha256()
+    for p in parts:
+        h.update(p if isinstance(p, bytes) else str(p).encode())
+    return h.hexdigest()
+
+
+def _file_sha(path) -> str:
+    with open(path, "rb") as fh:
+        return _sha(fh.read())
+
+
 def _compile(src, verbose=False, ptxas_info=False):
+    """Compile one .cu unless its object is current.  Staleness is keyed on a hash of
+    the source, every header it may include and the flags -- not on mtimes -- so a
+    copied, restored or half-written object is never mistaken for current."""
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-    deps = [src] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
+    deps = [src] + sorted(os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh"))
     deps.append(os.path.join(INCLUDE, "ndf_b200.h"))
-    if (not ptxas_info and os.path.exists(obj)
-            and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps)):
+    key = _sha(*[_file_sha(d) for d in deps], *ARCH, *FLAGS)
+    stamp = obj + ".sha"
+    if (not ptxas_info and os.path.exists(obj) and os.path.exists(stamp)
+            and open(stamp).read() == key + _file_sha(obj)):
         return obj, ""
     cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
     if ptxas_info:
@@ -51,6 +69,8 @@ def _compile(src, verbose=False, ptxas_info=False):
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
+    with open(stamp, "w") as fh:
+        fh.write(key + _file_sha(obj))
     return obj, res.stderr
 
 
@@ -63,14 +83,20 @@ def build(verbose=False, ptxas_info=False, force=False) -> str:
     if ptxas_info:
         for (o, log) in results:
             print(f"== {os.path.basename(o)}\n{log}")
-    if (force or not os.path.exists(LIB)
-            or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
+    # relink unless the library is byte-for-byte the one linked from these objects
+    key = _sha(*[_file_sha(o) for o in objs])
+    stamp = os.path.join(BUILD, "libndf_b200.sha")
+    current = (os.path.exists(LIB) and os.path.exists(stamp)
+               and open(stamp).read() == key + _file_sha(LIB))
+    if force or not current:
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+        with open(stamp, "w") as fh:
+            fh.write(key + _file_sha(LIB))
     return LIB
 
 

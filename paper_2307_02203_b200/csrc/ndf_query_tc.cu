@@ -1860,6 +1860,10 @@ extern "C" int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs,
   NDF_REQUIRE(m->tc_format == NDF_PREC_BF16 || m->tc_format == NDF_PREC_FP16, NDF_ERR_PARAMETER,
               "multi-reference queries run on the tensor-core path only");
   if (v0 == v1) return NDF_OK;
+  // device memory or page-locked host memory (written over PCIe); pageable refused
+  void* out_dev = nullptr;
+  st = resolve_output(out_f16, &out_dev);
+  if (st) return st;
   QueryArgs a{};
   a.m = *m;
   a.g = make_geom(*m);
@@ -1868,5 +1872,5 @@ extern "C" int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs,
   a.nx = nx; a.ny = ny; a.nz = nz;
   a.v0 = v0; a.v1 = v1;
   a.prec = m->tc_format;
-  return run_tc(a, refs, n_ref, out_f16, ld_out, as_stream(stream));
+  return run_tc(a, refs, n_ref, reinterpret_cast<uint16_t*>(out_dev), ld_out, as_stream(stream));
 }

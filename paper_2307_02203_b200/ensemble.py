@@ -196,7 +196,14 @@ def _as_device_positions(positions, device):
     return pos.contiguous()
 
 
+_FOREIGN_ENSEMBLES = {}   # (id(field), variable, device) -> (weakref, DeviceEnsemble)
+
+
 def _device_view(field_obj, variable: str, device=None) -> DeviceEnsemble:
+    """HBM view of one variable: a DeviceEnsemble, a {name: DeviceEnsemble} dict, this
+    package's EnsembleField (cached upload), or the reference's own
+    ``ndf.ensemble.EnsembleField`` (ensemble.py:65-112; duck-typed on ``domain`` and
+    ``member_grids``; immutable, so its upload is cached per object until it is freed)."""
     if isinstance(field_obj, DeviceEnsemble):
         return field_obj
     if isinstance(field_obj, dict):          # {name: DeviceEnsemble}
@@ -204,7 +211,32 @@ def _device_view(field_obj, variable: str, device=None) -> DeviceEnsemble:
             return field_obj[variable]
         except KeyError:
             raise UnknownVariableError(f"unknown variable {variable!r}") from None
-    return field_obj.to_device(variable, device)
+    if hasattr(field_obj, "to_device"):
+        return field_obj.to_device(variable, device)
+    if not (hasattr(field_obj, "member_grids") and hasattr(field_obj, "domain")):
+        raise ParameterError(f"not an ensemble field: {type(field_obj).__name__}")
+    import weakref
+    dev = N.require_cuda(device)
+    key = (id(field_obj), variable, str(dev))
+    hit = _FOREIGN_ENSEMBLES.get(key)
+    if hit is not None and hit[0]() is field_obj:
+        return hit[1]
+    try:
+        grids = field_obj.member_grids(variable)
+    except Exception as exc:                 # the reference raises its own UnknownVariableError
+        raise UnknownVariableError(str(exc)) from None
+    d = field_obj.domain
+    if tuple(np.shape(grids))[1:] != (d.nz, d.ny, d.nx):
+        raise DataError("member grids do not match the field's domain")
+    if not np.isfinite(grids).all():
+        raise DataError("ensemble contains non-finite values")
+    view = DeviceEnsemble.from_numpy(grids, device=dev)
+    try:
+        weakref.finalize(field_obj, _FOREIGN_ENSEMBLES.pop, key, None)
+        _FOREIGN_ENSEMBLES[key] = (weakref.ref(field_obj), view)
+    except TypeError:
+        pass
+    return view
 
 
 def sample_many(field_obj, variable: str, positions, chunk: int = 8192) -> np.ndarray:
@@ -298,6 +330,9 @@ def load_ensemble_device(path, variable: str, device=None, chunk_bytes: int = 25
         views = [memoryview(b.numpy()) for b in bufs]
         done = [None, None]
         stream = torch.cuda.Stream(dev)
+        # X came from the caching allocator on the current stream: a block it recycled
+        # may still be in use by work queued there, so the side stream waits for it
+        stream.wait_stream(torch.cuda.current_stream(dev))
         fh.seek(data_off + names.index(variable) * per_var)
         pos, i = 0, 0
         while pos < per_var:

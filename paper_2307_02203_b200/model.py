@@ -27,7 +27,7 @@ from dataclasses import asdict, dataclass, replace
 import numpy as np
 
 from . import _native as N
-from .errors import ConfigError, FormatError, ModelCorruptError, ShapeError
+from .errors import ConfigError, FormatError, ModelCorruptError, ParameterError, ShapeError
 
 NDFM_MAGIC = b"NDFM"
 NDFM_VERSION = 1
@@ -184,7 +184,7 @@ class NdfModel:
     """Instantiated NDF (model.py:105-142): host parameters + cached device state."""
 
     def __init__(self, spec: ModelSpec, grid_mu: np.ndarray, grid_nu: np.ndarray,
-                 weights: list, biases: list, enc_mu=None, enc_nu=None):
+                 weights: list, biases: list, enc_mu=None, enc_nu=None, _shared=None):
         C = spec.features_per_level
         if spec.shared and grid_mu is not grid_nu:
             raise ConfigError("shared spec requires aliased grids")
@@ -219,6 +219,9 @@ class NdfModel:
         self.weights = weights
         self.biases = biases
         self._dev = {}
+        # parameter-version record shared by every NdfModel over the same host arrays
+        # (with_precision copies): invalidate() on any of them retires all device copies
+        self._shared = _shared if _shared is not None else {"version": 0}
 
     @staticmethod
     def grid_shape(spec: ModelSpec) -> tuple:
@@ -278,24 +281,139 @@ class NdfModel:
                 raise ModelCorruptError("model contains non-finite parameters")
 
     def invalidate(self) -> None:
-        """Drop cached device copies (call after mutating parameters in place)."""
+        """Make the parameters writable again and retire every device copy made from
+        them (this model's and its with_precision siblings'): the next query re-validates
+        (validate_finite, as the reference does per call, service.py:58-59) and re-uploads.
+
+        Uploading freezes the host arrays (``writeable = False``): an in-place update --
+        the reference's Adam.step writes model.parameters() in place (nn.py:197-214) --
+        then raises instead of leaving the GPU copy silently stale."""
+        self._shared["version"] += 1
         self._dev.clear()
+        for p in self.parameters():
+            try:
+                p.flags.writeable = True
+            except ValueError:
+                pass               # a read-only base (e.g. a memory map) stays read-only
+
+    def _freeze(self) -> None:
+        for p in self.parameters():
+            p.flags.writeable = False
 
     def with_precision(self, precision: str) -> "NdfModel":
         """Same parameters, other query precision (shares host arrays)."""
         return NdfModel(replace(self.spec, precision=precision), self.grid_mu, self.grid_nu,
-                        self.weights, self.biases, self.enc_mu, self.enc_nu)
+                        self.weights, self.biases, self.enc_mu, self.enc_nu, _shared=self._shared)
 
     # -- device state -------------------------------------------------------
 
     def device_state(self, device=None) -> "DeviceModel":
         dev = N.require_cuda(device)
         key = str(dev)
-        if key not in self._dev:
+        st = self._dev.get(key)
+        if st is None or st.version != self._shared["version"]:
             self.spec.check_gpu_supported()
-            self.validate_finite()        # once per upload (SURVEY 5: failure detection)
-            self._dev[key] = DeviceModel(self, dev)
-        return self._dev[key]
+            # validated once per upload; the arrays are frozen until invalidate(), so a
+            # per-call re-check (service.py:58-59) could not find anything new
+            self.validate_finite()
+            st = DeviceModel(self, dev)
+            self._freeze()
+            st.version = self._shared["version"]
+            self._dev[key] = st
+        return st
+
+    # -- embedding ----------------------------------------------------------
+
+    def _branch(self, grid) -> int:
+        if grid is self.grid_mu or (isinstance(grid, str) and grid == "mu"):
+            return 0
+        if grid is self.grid_nu or (isinstance(grid, str) and grid == "nu"):
+            return 1
+        tables = getattr(grid, "tables", None)          # a reference HashGrid
+        if tables is not None:
+            for b, mine in ((0, self.grid_mu), (1, self.grid_nu)):
+                if tables is mine or (tables.shape == mine.shape and np.array_equal(tables, mine)):
+                    return b
+        raise ParameterError("grid must be this model's grid_mu / grid_nu (or 'mu' / 'nu')")
+
+    def embed(self, grid, positions) -> np.ndarray:
+        """model.py:169-177 -- [raw(3) | fourier(6L) | latent] per position, computed in
+        fp64 and cast to fp32 on the GPU (ndf_embed_points), bit-identical to the reference.
+        ``grid`` is this model's grid_mu / grid_nu (or "mu" / "nu")."""
+        import torch
+        branch = self._branch(grid)
+        pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+        if pos.ndim != 2 or pos.shape[1] != 3:
+            raise ShapeError(f"positions must be (B, 3), got {pos.shape}")
+        st = self.device_state()
+        out = torch.empty((pos.shape[0], self.spec.embed_dim), dtype=torch.float32,
+                          device=st.device)
+        if pos.shape[0]:
+            dpos = torch.from_numpy(np.ascontiguousarray(pos)).to(st.device)
+            N.call("ndf_embed_points", ctypes_ref(st.desc), branch, N.ptr(dpos), pos.shape[0],
+                   N.ptr(out), N.stream_handle(st.device))
+        return out.cpu().numpy()
+
+    def embed_nodes(self, grid, dims, v0: int = 0, v1: int | None = None):
+        """Embeddings of output-grid nodes [v0, v1) of ``dims`` (x fastest,
+        measures.py:240-252) as a (v1 - v0, E) float32 CUDA tensor (ndf_embed_nodes)."""
+        import torch
+        branch = self._branch(grid)
+        dims = tuple(int(d) for d in dims)
+        if len(dims) != 3 or min(dims) < 1:
+            raise ParameterError(f"grid dims must be >= 1, got {dims}")
+        V = dims[0] * dims[1] * dims[2]
+        v1 = V if v1 is None else int(v1)
+        if not 0 <= v0 <= v1 <= V:
+            raise ParameterError("vertex range out of bounds")
+        st = self.device_state()
+        out = torch.empty((v1 - v0, self.spec.embed_dim), dtype=torch.float32, device=st.device)
+        N.call("ndf_embed_nodes", ctypes_ref(st.desc), branch, dims[0], dims[1], dims[2], v0, v1,
+               N.ptr(out), N.stream_handle(st.device))
+        return out
+
+    # -- the reference's own model objects -------------------------------------
+
+    @classmethod
+    def from_reference(cls, ref, precision: str = "fp32") -> "NdfModel":
+        """Convert the reference's ``ndf.model.NdfModel`` (HashGrid / Mlp objects,
+        model.py:105-142) -- duck-typed on ``spec``, ``grid_mu.tables``, ``enc_mu.weights``
+        and ``decoder.weights`` -- into this package's model.  The parameters are copied
+        (a snapshot: training the reference object later does not touch this one; see
+        ``as_model`` for the cached, change-detecting form).  A single dense level with
+        no encoder becomes the dense layout, like an NDFM file (load_model); the
+        reference family keeps its HashGrid tables and encoders (exact fp32 kernel)."""
+        if isinstance(ref, NdfModel):
+            return ref
+        try:
+            rspec = ref.spec
+            names = [f for f in ModelSpec.__dataclass_fields__ if hasattr(rspec, f)]
+            fields = {f: getattr(rspec, f) for f in names}
+            acts = {ref.decoder.act}
+            if ref.enc_mu.weights:
+                acts |= {ref.enc_mu.act, ref.enc_nu.act}
+        except AttributeError as exc:
+            raise ConfigError(f"not a reference NdfModel: {exc}") from None
+        if len(acts) != 1:
+            raise ConfigError(f"mixed encoder / decoder activations {sorted(acts)} are not supported")
+        fields.update(activation=acts.pop(), head="linear", precision=precision,
+                      grid_resolution=None)
+        spec = ModelSpec(**fields)
+        cp = lambda a: np.array(a, dtype=np.float32, copy=True)   # noqa: E731
+        t_mu = cp(ref.grid_mu.tables)
+        t_nu = t_mu if spec.shared else cp(ref.grid_nu.tables)
+        if not spec.hash_grid:
+            rx, ry, rz = spec.latent_resolution
+            C = spec.features_per_level
+            t_mu = t_mu[0][: rx * ry * rz].reshape(rz, ry, rx, C).copy()
+            t_nu = t_mu if spec.shared else t_nu[0][: rx * ry * rz].reshape(rz, ry, rx, C).copy()
+
+        def mlp(m):
+            return [cp(w) for w in m.weights], [cp(b) for b in m.biases]
+        enc_mu = mlp(ref.enc_mu)
+        enc_nu = enc_mu if spec.shared else mlp(ref.enc_nu)
+        ws, bs = mlp(ref.decoder)
+        return cls(spec, t_mu, t_nu, ws, bs, enc_mu, enc_nu)
 
     # -- forward ------------------------------------------------------------
 
@@ -331,6 +449,52 @@ class NdfModel:
 
     def forward_pair(self, p_mu, p_nu) -> float:
         return float(self.forward(np.reshape(p_mu, (1, 3)), np.reshape(p_nu, (1, 3)))[0])
+
+
+_FOREIGN = {}          # id(reference model) -> (fingerprint, converted NdfModel)
+
+
+def _fingerprint(arrays) -> tuple:
+    """Cheap content key of a parameter list: identity, shape and two 64-bit folds of
+    the bytes (sum and xor) -- an in-place training step changes it."""
+    key = []
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        u = a.reshape(-1).view(np.uint8)
+        pad = (-u.size) % 8
+        if pad:
+            u = np.concatenate([u, np.zeros(pad, np.uint8)])
+        w = u.view(np.uint64)
+        key.append((a.shape, str(a.dtype), int(np.add.reduce(w, dtype=np.uint64)),
+                    int(np.bitwise_xor.reduce(w)) if w.size else 0))
+    return tuple(key)
+
+
+def as_model(model, precision: str | None = None) -> NdfModel:
+    """This package's NdfModel for ``model``: itself, or the conversion of a reference
+    ``ndf.model.NdfModel`` (NdfModel.from_reference), cached per object and rebuilt
+    when the reference's parameters change (the reference trains in place,
+    nn.py:197-214).  ``precision`` applies to converted models (default fp32, the
+    reference's own arithmetic)."""
+    if isinstance(model, NdfModel):
+        return model
+    import weakref
+    params = model.parameters() if hasattr(model, "parameters") else None
+    if params is None:
+        raise ConfigError(f"not an NDF model: {type(model).__name__}")
+    fp = _fingerprint(params)
+    key = (id(model), precision or "fp32")
+    hit = _FOREIGN.get(key)
+    if hit is not None and hit[0] == fp and hit[2]() is model:
+        return hit[1]
+    conv = NdfModel.from_reference(model, precision or "fp32")
+    try:
+        ref = weakref.ref(model)
+        weakref.finalize(model, _FOREIGN.pop, key, None)
+    except TypeError:                      # not weak-referenceable: do not cache
+        return conv
+    _FOREIGN[key] = (fp, conv, ref)
+    return conv
 
 
 def ctypes_ref(desc):

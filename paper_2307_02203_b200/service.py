@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .errors import NotFoundError, ParameterError
 from .measures import CorrelationMeasure, FieldGrid, ground_truth_field
-from .model import NdfModel, ctypes_ref
+from .model import NdfModel, as_model, ctypes_ref
 
 DEFAULT_QUERY_BATCH = 65536
 ROLE_MU = "reference-is-mu"
@@ -50,6 +50,7 @@ def reconstruct_field_device(model: NdfModel, ref, role: str = ROLE_MU, dims=(64
     """
     import torch
     _check_role(role)
+    model = as_model(model)
     dims = _check_dims(dims)
     V = dims[0] * dims[1] * dims[2]
     v1 = V if v1 is None else int(v1)
@@ -59,6 +60,8 @@ def reconstruct_field_device(model: NdfModel, ref, role: str = ROLE_MU, dims=(64
     ref = np.asarray(ref, dtype=np.float64).reshape(3)
     if out is None:
         out = torch.empty(v1 - v0, dtype=torch.float32, device=st.device)
+    else:
+        _check_out(out, torch.float32, (v1 - v0,), st.device)
     N.call("ndf_query_grid", st.desc_ref, float(ref[0]), float(ref[1]), float(ref[2]),
            1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], v0, v1,
            N.PREC[model.spec.precision], out.data_ptr(),
@@ -70,10 +73,33 @@ def reconstruct_field_device(model: NdfModel, ref, role: str = ROLE_MU, dims=(64
     return out
 
 
+def _check_out(out, dtype, shape, device) -> None:
+    """Caller-supplied output buffers: the kernels write exactly ``shape`` elements
+    through the raw pointer, so anything else is refused before the launch."""
+    import torch
+    if not isinstance(out, torch.Tensor) or out.dtype != dtype:
+        raise ParameterError(f"out must be a {dtype} tensor")
+    if len(shape) == 1:
+        if not out.is_contiguous() or out.numel() < shape[0]:
+            raise ParameterError(f"out must be contiguous with >= {shape[0]} elements")
+    else:
+        if (out.dim() != 2 or out.shape[0] < shape[0] or out.shape[1] < shape[1]
+                or out.stride(1) != 1):
+            raise ParameterError(f"out must be a row-major {shape[0]} x {shape[1]} (or larger) "
+                                 "tensor")
+    if out.is_cuda:
+        if out.device != device:
+            raise ParameterError(f"out is on {out.device}, the model on {device}")
+    elif not out.is_pinned():
+        raise ParameterError("out must be CUDA memory or pinned host memory")
+
+
 def reconstruct_field(model: NdfModel, ref, role: str = ROLE_MU, dims=(64, 64, 64),
                       batch_size: int = DEFAULT_QUERY_BATCH, clamp: bool = False) -> FieldGrid:
-    """service.py:46-84 -- dependence field of ``ref`` over the output grid."""
+    """service.py:46-84 -- dependence field of ``ref`` over the output grid.  ``model``
+    is this package's NdfModel or the reference's own (converted once, as_model)."""
     _check_role(role)
+    model = as_model(model)
     if batch_size < 1:
         raise ParameterError("batch_size must be >= 1")
     dims = _check_dims(dims)
@@ -116,6 +142,7 @@ def to_host(t) -> np.ndarray:
 def difference_field(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,
                      batch_size: int = DEFAULT_QUERY_BATCH) -> FieldGrid:
     """service.py:87-94."""
+    model = as_model(model)
     fa = reconstruct_field_device(model, ref_a, role, dims)
     fb = reconstruct_field_device(model, ref_b, role, dims)
     return FieldGrid(_check_dims(dims), (fa - fb).cpu().numpy())
@@ -124,6 +151,7 @@ def difference_field(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,
 def matrix_reconstruct(models: list, variables: list, ref, dims,
                        batch_size: int = DEFAULT_QUERY_BATCH) -> list:
     """service.py:97-125 -- all d*d fields for one reference point, row-major."""
+    models = [as_model(m) for m in models]
     by_pair = {(m.spec.var_mu, m.spec.var_nu): m for m in models}
     missing = []
     for i, vi in enumerate(variables):
@@ -173,6 +201,7 @@ def benchmark(model: NdfModel, field_obj, ref, dims, repetitions: int = 3, k: in
               mi_points: int = 1024) -> BenchmarkReport:
     """service.py:186-220 -- median wall clock of NDF vs direct estimators (GPU)."""
     import torch
+    model = as_model(model)
     if repetitions < 1:
         raise ParameterError("repetitions must be >= 1")
     dims = _check_dims(dims)
@@ -214,6 +243,7 @@ def reconstruct_multi_device(model: NdfModel, refs, role: str = ROLE_MU, dims=(6
     """
     import torch
     _check_role(role)
+    model = as_model(model)
     dims = _check_dims(dims)
     V = dims[0] * dims[1] * dims[2]
     v1 = V if v1 is None else int(v1)
@@ -228,9 +258,15 @@ def reconstruct_multi_device(model: NdfModel, refs, role: str = ROLE_MU, dims=(6
     drefs = torch.from_numpy(refs_np).to(st.device)
     if out is None:
         out = torch.empty((n_ref, v1 - v0), dtype=torch.float16, device=st.device)
-    if out.dtype != torch.float16 or out.shape[0] < n_ref or out.stride(1) != 1:
-        raise ParameterError("out must be a row-major float16 tensor with >= n_ref rows")
+    else:
+        _check_out(out, torch.float16, (n_ref, v1 - v0), st.device)
     N.call("ndf_query_grid_multi", ctypes_ref(st.desc), N.ptr(drefs), n_ref,
            1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], v0, v1, N.ptr(out),
            out.stride(0), N.stream_handle(st.device))
     return out
+
+
+def forward(model, p_mu, p_nu, exact: bool = True) -> np.ndarray:
+    """NdfModel.forward (model.py:179-189) for this package's models or the reference's
+    own (as_model): batched dependence estimates, shape (B,) float32."""
+    return as_model(model).forward(p_mu, p_nu, exact)

@@ -1,0 +1,92 @@
+"""The drop-in boundary against the reference's own objects (VERDICT r1 missing #3), CPU.
+
+NdfModel.from_reference / as_model convert the unmodified reference's
+``ndf.model.NdfModel`` (built here from /root/reference with its own RNG) with the
+parameters copied bit for bit; a changed reference model is re-converted.  The GPU side
+(reconstruct_field / forward / ground_truth_field / embed on reference-structured objects)
+is tests/test_gpu_dropin.py."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2307_02203_b200 as ndf
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.fixture(scope="module")
+def refndf():
+    if not os.path.isdir(REF_SRC):
+        pytest.skip("reference package not present (GPU box)")
+    sys.path.insert(0, REF_SRC)
+    try:
+        import ndf as reference
+        from ndf import model as rmodel
+    finally:
+        sys.path.remove(REF_SRC)
+    return reference, rmodel
+
+
+def _same_params(ours, theirs):
+    a, b = ours.parameters(), theirs.parameters()
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert x.dtype == np.float32
+        assert np.array_equal(x.reshape(-1), np.asarray(y).reshape(-1))
+
+
+def test_reference_default_model_converts_bitwise(refndf):
+    _, rmodel = refndf
+    ref = rmodel.NdfModel.build(rmodel.ModelSpec(), seed=3)
+    ours = ndf.NdfModel.from_reference(ref)
+    assert ours.spec.hash_grid and ours.spec.activation == "snake_alt"
+    assert ours.spec.head_kind == "linear" and ours.spec.merge == "multiply"
+    assert ours.spec.decoder_widths() == ref.spec.decoder_widths()
+    assert ours.spec.encoder_widths() == ref.spec.encoder_widths()
+    _same_params(ours, ref)
+    # the copy is a snapshot: our arrays are not the reference's
+    assert not np.shares_memory(ours.grid_mu, ref.grid_mu.tables)
+    # and equals what the reference's own NDFM file loads as
+    assert ours.spec == ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=3).spec
+
+
+def test_unshared_and_dense_reference_models(refndf, tmp_path):
+    _, rmodel = refndf
+    spec = rmodel.ModelSpec(var_mu="a", var_nu="b", merge="concat", levels=1,
+                            base_resolution=8, log2_table_size=9, features_per_level=4,
+                            encoder_layers=0, channels=16)
+    ref = rmodel.NdfModel.build(spec, seed=5)
+    ours = ndf.NdfModel.from_reference(ref)
+    assert not ours.spec.hash_grid and ours.grid_mu.shape == (8, 8, 8, 4)
+    path = tmp_path / "m.ndfm"
+    rmodel.save_model(ref, path)
+    loaded = ndf.load_model(path)          # the reference's own file, our loader
+    for x, y in zip(ours.parameters(), loaded.parameters()):
+        assert np.array_equal(x, y)
+
+
+def test_as_model_caches_and_detects_training_updates(refndf):
+    _, rmodel = refndf
+    ref = rmodel.NdfModel.build(rmodel.ModelSpec(), seed=1)
+    a = ndf.as_model(ref)
+    assert ndf.as_model(ref) is a
+    ref.decoder.biases[0][0] += 0.25          # an in-place training update
+    b = ndf.as_model(ref)
+    assert b is not a
+    assert b.biases[0][0] == ref.decoder.biases[0][0] != a.biases[0][0]
+    assert ndf.as_model(b) is b
+
+
+def test_stand_in_objects_match_the_reference_structure(refndf):
+    """tests/refobjects.py (used on the GPU box) converts like the real objects."""
+    import refobjects
+    _, rmodel = refndf
+    ref = rmodel.NdfModel.build(rmodel.ModelSpec(), seed=2)
+    ours = ndf.NdfModel.from_reference(ref)
+    again = ndf.NdfModel.from_reference(refobjects.ref_model_like(ours))
+    assert again.spec == ours.spec
+    for x, y in zip(ours.parameters(), again.parameters()):
+        assert np.array_equal(x, y)

@@ -400,3 +400,55 @@ def test_reference_default_vs_oracle_c0_grid():
         got = ndf.reconstruct_field(m, ref, role, dims).values
         want = O.reconstruct_field(om, ref, dims, role=role)
         assert np.max(np.abs(got - want)) <= 1e-5
+
+
+def test_output_buffers_are_checked(c0):
+    """Caller-supplied outputs: wrong dtype, too short, non-contiguous,
+    another device or pageable host memory are refused before any launch."""
+    w, model = c0
+    ref = w.ref_position()
+    V = w.n_vertices
+    for bad in (torch.empty(V, dtype=torch.float16, device="cuda"),
+                torch.empty(V - 1, dtype=torch.float32, device="cuda"),
+                torch.empty(2 * V, dtype=torch.float32, device="cuda")[::2],
+                torch.empty(V, dtype=torch.float32)):                 # pageable host
+        with pytest.raises(ndf.ParameterError):
+            ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, w.dims, out=bad)
+    m16 = model.with_precision("fp16")
+    refs = np.array([ref, (0.1, 0.2, 0.3)])
+    for bad in (torch.empty((2, V), dtype=torch.float16),             # pageable host
+                torch.empty((2, V - 1), dtype=torch.float16, device="cuda"),
+                torch.empty((1, V), dtype=torch.float16, device="cuda"),
+                torch.empty((2, V), dtype=torch.float32, device="cuda")):
+        with pytest.raises(ndf.ParameterError):
+            ndf.reconstruct_multi_device(m16, refs, ndf.ROLE_MU, w.dims, out=bad)
+    # pinned host cube: written by the kernel over PCIe, equal to the device cube
+    pinned = torch.empty((2, V), dtype=torch.float16, pin_memory=True)
+    ndf.reconstruct_multi_device(m16, refs, ndf.ROLE_MU, w.dims, out=pinned)
+    torch.cuda.synchronize()
+    assert torch.equal(pinned, ndf.reconstruct_multi_device(m16, refs, ndf.ROLE_MU, w.dims).cpu())
+
+
+def test_uploaded_parameters_are_frozen_until_invalidate():
+    """in-place edits after upload raise instead of going stale; invalidate()
+    re-enables them, re-validates (NaN -> ModelCorruptError) and re-uploads for every
+    model sharing the arrays (with_precision siblings included)."""
+    w = W.CONFIGS[0]
+    model = W.build_model(w, seed=0, grid_init=1.0)
+    m16 = model.with_precision("fp16")
+    ref = w.ref_position()
+    a = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims).values
+    a16 = ndf.reconstruct_field(m16, ref, ndf.ROLE_MU, w.dims).values
+    with pytest.raises(ValueError):
+        model.biases[-1][0] = 0.5
+    model.invalidate()
+    model.biases[-1][0] = 0.5                 # now writable; both models re-upload
+    b = ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims).values
+    b16 = ndf.reconstruct_field(m16, ref, ndf.ROLE_MU, w.dims).values
+    assert not np.array_equal(a, b) and not np.array_equal(a16, b16)
+    om = oracle_model(model)
+    assert np.max(np.abs(b - O.reconstruct_field(om, ref, w.dims))) <= TOL32
+    model.invalidate()
+    model.weights[0][0, 0] = np.nan
+    with pytest.raises(ndf.ModelCorruptError):
+        ndf.reconstruct_field(m16, ref, ndf.ROLE_MU, w.dims)
