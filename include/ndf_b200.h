@@ -151,6 +151,24 @@ int ndf_query_grid_multi(const ndf_model_desc* m, const double* refs, int32_t n_
 int ndf_sample_many(const float* X, int32_t M, int32_t nx, int32_t ny, int32_t nz,
                     const double* pos, int64_t B, double* out, void* stream);
 
+/* sample_many over a column window: X holds node columns [col0, col0 + ld) of the
+ * member-major ensemble with member rows ld elements apart (a V-slice on one GPU of a
+ * sharded ensemble); every sampled lattice corner must lie inside the window.
+ * ndf_sample_many == ndf_sample_many_ld with ld = nx*ny*nz, col0 = 0. */
+int ndf_sample_many_ld(const float* X, int32_t M, int64_t ld, int64_t col0, int32_t nx,
+                       int32_t ny, int32_t nz, const double* pos, int64_t B, double* out,
+                       void* stream);
+
+/* Ground-truth Pearson field in ONE streaming read of X: out[v - v0] = pearson of node
+ * column v against ref_vec (fp64, M; device) for v in [v0, v1) -- measures.py:84-108 over
+ * a node-aligned ground_truth_field (measures.py:286-295): fp64 shifted moments per
+ * column, NaN where either side is degenerate, exactly 1.0 for a column equal to the
+ * reference, clipped to [-1, 1].  X is a column window as for ndf_sample_many_ld
+ * (col0 <= v0 <= v1 <= col0 + ld).  No standardised copy is built; the reference
+ * statistics are computed on the device (no host round trip). */
+int ndf_pearson_field(const float* X, int32_t M, int64_t ld, int64_t col0,
+                      const double* ref_vec, int64_t v0, int64_t v1, float* out, void* stream);
+
 /* Per-vertex standardisation (one-time prep of the Pearson GEMV):
  * Z[m][v] = (X[m][v] - mean_v) / sqrt(sum_m (X - mean_v)^2) in fp64 -> fp32;
  * norm[v] = that sqrt (0 marks a degenerate vertex).  Vertices [v0, v1). */

@@ -37,9 +37,11 @@ __device__ __forceinline__ void frac_index(double p, int n, int& i0, double& t) 
   i0 = i;
 }
 
-__global__ void sample_many_kernel(const float* __restrict__ X, int M, int nx, int ny, int nz,
-                                   const double* __restrict__ pos, int64_t B,
-                                   double* __restrict__ out) {
+// X holds node columns [col0, col0 + ld) of the member-major ensemble, member rows
+// ld apart (ld = V, col0 = 0: the whole variable).
+__global__ void sample_many_kernel(const float* __restrict__ X, int M, int64_t ld, int64_t col0,
+                                   int nx, int ny, int nz, const double* __restrict__ pos,
+                                   int64_t B, double* __restrict__ out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * (int64_t)M) return;
   const int64_t b = idx / M;
@@ -49,8 +51,7 @@ __global__ void sample_many_kernel(const float* __restrict__ X, int M, int nx, i
   frac_index(pos[3 * b + 0], nx, ix, tx);
   frac_index(pos[3 * b + 1], ny, iy, ty);
   frac_index(pos[3 * b + 2], nz, iz, tz);
-  const int64_t V = (int64_t)nx * ny * nz;
-  const float* g = X + (int64_t)m * V;
+  const float* g = X + (int64_t)m * ld - col0;
   double acc = 0.0;
 #pragma unroll
   for (int dz = 0; dz < 2; ++dz) {
@@ -68,6 +69,135 @@ __global__ void sample_many_kernel(const float* __restrict__ X, int M, int nx, i
     }
   }
   out[idx] = acc;
+}
+
+// ---- fused Pearson field: one streaming read of X ---------------------------
+// r[v] = sum_m (x_mv - mu_v)(ref_m - mu_r) / sqrt(var_v * var_r), measures.py:84-108,
+// computed per vertex in ONE pass over its member column: shifted fp64 moments
+// (d = x - x_0v: sum d, sum d^2, sum d * rc_m with rc = ref - mean(ref) in fp64), so
+// neither Z nor a second read exists -- the bytes are exactly the column reads of X.
+// Rules of the reference: degenerate (var == 0 on either side) -> NaN (the field maps
+// it to 0 with a warning, measures.py:291-295); a column equal to the reference member
+// for member -> exactly 1.0 (measures.py:102-107); otherwise clipped to [-1, 1].
+constexpr int kFieldMaxM = 8192;
+
+struct RefStats {
+  double var_ref;     // sum (ref - mean)^2, fp64 two-pass
+  int exact32;        // every ref_m is an fp32 value (a node column can equal it)
+};
+
+// one block: rc_m = ref_m - mean(ref) (fp64, two-pass), r32 = (float)ref, var_ref
+__global__ void __launch_bounds__(1024)
+pearson_ref_kernel(const double* __restrict__ ref, int M, double* __restrict__ rc,
+                   float* __restrict__ r32, RefStats* __restrict__ st) {
+  __shared__ double red[32];
+  __shared__ int ok32[32];
+  auto block_sum = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+      t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    t = red[0];
+    __syncthreads();
+    return t;
+  };
+  double s = 0.0;
+  int ex = 1;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const double r = ref[m];
+    s += r;
+    ex &= ((double)(float)r == r);
+  }
+  const double mean = block_sum(s) / (double)M;
+  ex = __all_sync(0xffffffffu, ex);
+  if ((threadIdx.x & 31) == 0) ok32[threadIdx.x >> 5] = ex;
+  double q = 0.0;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const double c = ref[m] - mean;
+    rc[m] = c;
+    r32[m] = (float)ref[m];
+    q += c * c;
+  }
+  const double var = block_sum(q);
+  if (threadIdx.x == 0) {
+    int all = 1;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) all &= ok32[w];
+    st->var_ref = var;
+    st->exact32 = all;
+  }
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(256)
+pearson_field_kernel(const float* __restrict__ X, int M, int64_t ld, int64_t col0,
+                     const double* __restrict__ rc_g, const float* __restrict__ r32_g,
+                     const RefStats* __restrict__ st, int64_t v0, int64_t v1,
+                     float* __restrict__ out) {
+  extern __shared__ double rcs[];
+  float* r32 = reinterpret_cast<float*>(rcs + M);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    rcs[i] = rc_g[i];
+    r32[i] = r32_g[i];
+  }
+  __syncthreads();
+  const double var_ref = st->var_ref;
+  const bool can_eq = st->exact32 != 0;
+  const int64_t v = v0 + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (v >= v1) return;
+  const int nv = (int)min((int64_t)4, v1 - v);
+  const float* col = X + (v - col0);
+  double sd[4] = {0.0, 0.0, 0.0, 0.0}, sd2[4] = {0.0, 0.0, 0.0, 0.0}, sdr[4] = {0.0, 0.0, 0.0, 0.0};
+  float x0[4];
+  bool eq[4] = {can_eq, can_eq, can_eq, can_eq};
+  if (kVec && nv == 4) {
+    const float4 f = ld_stream4(col);
+    x0[0] = f.x; x0[1] = f.y; x0[2] = f.z; x0[3] = f.w;
+#pragma unroll 4
+    for (int m = 0; m < M; ++m) {
+      const float4 x4 = ld_stream4(col + (int64_t)m * ld);
+      const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+      const double r = rcs[m];
+      const float rr = r32[m];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double d = (double)xs[i] - (double)x0[i];
+        sd[i] += d;
+        sd2[i] = fma(d, d, sd2[i]);
+        sdr[i] = fma(d, r, sdr[i]);
+        eq[i] &= (xs[i] == rr);
+      }
+    }
+  } else {
+    for (int i = 0; i < nv; ++i) {
+      x0[i] = __ldg(col + i);
+      for (int m = 0; m < M; ++m) {
+        const float x = __ldg(col + (int64_t)m * ld + i);
+        const double d = (double)x - (double)x0[i];
+        sd[i] += d;
+        sd2[i] = fma(d, d, sd2[i]);
+        sdr[i] = fma(d, rcs[m], sdr[i]);
+        eq[i] &= (x == r32[m]);
+      }
+    }
+  }
+  for (int i = 0; i < nv; ++i) {
+    const double var = sd2[i] - sd[i] * (sd[i] / (double)M);
+    float r;
+    if (!(var_ref > 0.0) || !(var > 0.0)) {
+      r = __int_as_float(0x7fc00000);        // degenerate: NaN (measures.py:94-100)
+    } else if (eq[i]) {
+      r = 1.0f;                               // measures.py:102-107
+    } else {
+      r = (float)fmin(1.0, fmax(-1.0, sdr[i] / sqrt(var * var_ref)));
+    }
+    out[v + i - v0] = r;
+  }
 }
 
 // ---- z-score prep -----------------------------------------------------------
@@ -269,18 +399,71 @@ __global__ void transpose_kernel(const float* __restrict__ X, int M, int64_t V,
 
 using namespace ndf;
 
-extern "C" int ndf_sample_many(const float* X, int32_t M, int32_t nx, int32_t ny, int32_t nz,
-                               const double* pos, int64_t B, double* out, void* stream) {
+extern "C" int ndf_sample_many_ld(const float* X, int32_t M, int64_t ld, int64_t col0, int32_t nx,
+                                  int32_t ny, int32_t nz, const double* pos, int64_t B, double* out,
+                                  void* stream) {
   NDF_REQUIRE(M >= 1 && nx >= 2 && ny >= 2 && nz >= 2, NDF_ERR_PARAMETER,
               "sample_many: need M >= 1 and >= 2 nodes per axis");
   NDF_REQUIRE(B >= 0, NDF_ERR_PARAMETER, "negative batch");
+  NDF_REQUIRE(ld >= 1 && col0 >= 0, NDF_ERR_PARAMETER, "bad column window");
   if (B == 0) return NDF_OK;
   NDF_REQUIRE(X && pos && out, NDF_ERR_PARAMETER, "null pointer");
   const int64_t n = B * (int64_t)M;
   const int threads = 256;
   sample_many_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
-      X, M, nx, ny, nz, pos, B, out);
+      X, M, ld, col0, nx, ny, nz, pos, B, out);
   NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_sample_many(const float* X, int32_t M, int32_t nx, int32_t ny, int32_t nz,
+                               const double* pos, int64_t B, double* out, void* stream) {
+  return ndf_sample_many_ld(X, M, (int64_t)nx * ny * nz, 0, nx, ny, nz, pos, B, out, stream);
+}
+
+extern "C" int ndf_pearson_field(const float* X, int32_t M, int64_t ld, int64_t col0,
+                                 const double* ref_vec, int64_t v0, int64_t v1, float* out,
+                                 void* stream) {
+  NDF_REQUIRE(M >= 1 && M <= kFieldMaxM, NDF_ERR_UNSUPPORTED,
+              "pearson_field: M must be in [1, 8192]");
+  NDF_REQUIRE(ld >= 1 && col0 >= 0 && col0 <= v0 && v0 <= v1 && v1 <= col0 + ld,
+              NDF_ERR_PARAMETER, "vertex range outside the ensemble's column window");
+  if (v0 == v1) return NDF_OK;
+  NDF_REQUIRE(X && ref_vec && out, NDF_ERR_PARAMETER, "null pointer");
+  void* out_dev = nullptr;
+  int st = resolve_output(out, &out_dev);
+  if (st) return st;
+  void* scratch = nullptr;
+  NDF_CUDA_CHECK(scratch_alloc(&scratch, (size_t)M * 12 + 64, as_stream(stream)));
+  RefStats* rs = reinterpret_cast<RefStats*>(scratch);
+  double* rc = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(scratch) + 64);
+  float* r32 = reinterpret_cast<float*>(rc + M);
+  pearson_ref_kernel<<<1, 1024, 0, as_stream(stream)>>>(ref_vec, M, rc, r32, rs);
+  cudaError_t e = cudaGetLastError();
+  count_launch();
+  if (e == cudaSuccess) {
+    const int threads = 256;
+    const int64_t nthreads = (v1 - v0 + 3) / 4;
+    const unsigned blocks = (unsigned)((nthreads + threads - 1) / threads);
+    const size_t smem = (size_t)M * 12;
+    const bool vec = (ld % 4 == 0) && ((v0 - col0) % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    static SmemAttrCache attr;
+    e = attr.ensure(pearson_field_kernel<true>, (size_t)kFieldMaxM * 12);
+    if (e == cudaSuccess) e = attr.ensure(pearson_field_kernel<false>, (size_t)kFieldMaxM * 12);
+    if (e == cudaSuccess) {
+      if (vec)
+        pearson_field_kernel<true><<<blocks, threads, smem, as_stream(stream)>>>(
+            X, M, ld, col0, rc, r32, rs, v0, v1, static_cast<float*>(out_dev));
+      else
+        pearson_field_kernel<false><<<blocks, threads, smem, as_stream(stream)>>>(
+            X, M, ld, col0, rc, r32, rs, v0, v1, static_cast<float*>(out_dev));
+      e = cudaGetLastError();
+      count_launch();
+    }
+  }
+  cudaFreeAsync(scratch, as_stream(stream));
+  NDF_CUDA_CHECK(e);
   return NDF_OK;
 }
 

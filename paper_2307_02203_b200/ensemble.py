@@ -109,21 +109,51 @@ class DeviceEnsemble:
     """One variable's ensemble resident on a CUDA device, member-major fp32.
 
     ``X`` is a torch tensor of shape (M, nz, ny, nx) -- the NDFE payload layout,
-    so member rows are contiguous over vertices (coalesced GEMV / KSG loads).
+    so member rows are contiguous over vertices (coalesced GEMV / KSG loads) -- or,
+    for a V-slice of a sharded ensemble, (M, cols) holding node columns
+    [col0, col0 + cols) of the same layout (``window``).
     """
 
-    def __init__(self, X, domain: GridDomain):
+    def __init__(self, X, domain: GridDomain, col0: int = 0):
         import torch
-        if X.dtype != torch.float32 or X.dim() != 4 or not X.is_cuda:
-            raise DataError("DeviceEnsemble needs a (M, nz, ny, nx) float32 CUDA tensor")
-        M, nz, ny, nx = X.shape
-        if (nx, ny, nz) != domain.dims:
-            raise DataError("tensor shape does not match domain")
+        if X.dtype != torch.float32 or not X.is_cuda:
+            raise DataError("DeviceEnsemble needs a float32 CUDA tensor")
+        if X.dim() == 4:
+            M, nz, ny, nx = X.shape
+            if (nx, ny, nz) != domain.dims or col0 != 0:
+                raise DataError("tensor shape does not match domain")
+        elif X.dim() != 2 or col0 < 0 or col0 + X.shape[1] > domain.node_count:
+            raise DataError("column window must be (M, cols) inside the domain")
         self.X = X.contiguous()
         self.domain = domain
+        self.col0 = int(col0)
+        self.ld = int(X.shape[1]) if X.dim() == 2 else domain.node_count
         self._z = None
         self._norm = None
         self._xv = None
+
+    @classmethod
+    def window(cls, grids, c0: int, c1: int, device=None) -> "DeviceEnsemble":
+        """Upload node columns [c0, c1) of host member grids (N, nz, ny, nx): the V-slice
+        one rank of a sharded ensemble holds (0.88 GB per GPU for config 1 at 8 GPUs)."""
+        import torch
+        dev = N.require_cuda(device)
+        g = np.asarray(grids)
+        if g.ndim != 4:
+            raise DataError("member grids must be (N, nz, ny, nx)")
+        dom = GridDomain(g.shape[3], g.shape[2], g.shape[1])
+        if not 0 <= c0 < c1 <= dom.node_count:
+            raise ParameterError("column window out of range")
+        cols = np.ascontiguousarray(g.reshape(g.shape[0], -1)[:, c0:c1], dtype=np.float32)
+        return cls(torch.from_numpy(cols).to(dev), dom, c0)
+
+    @property
+    def full(self) -> bool:
+        return self.col0 == 0 and self.ld == self.domain.node_count
+
+    def _need_full(self, what):
+        if not self.full:
+            raise ParameterError(f"{what} needs the whole variable, not a column window")
 
     @classmethod
     def from_numpy(cls, grids: np.ndarray, device=None) -> "DeviceEnsemble":
@@ -150,6 +180,7 @@ class DeviceEnsemble:
     def zscore(self):
         """(Z, norm): standardised copy for the Pearson GEMV, built once (ndf_zscore)."""
         import torch
+        self._need_full("zscore")
         if self._z is None:
             M, V = self.member_count, self.node_count
             Z = torch.empty((M, V), dtype=torch.float32, device=self.device)
@@ -162,6 +193,7 @@ class DeviceEnsemble:
     def vertex_major(self):
         """(V, M) copy for pair lists, built once (ndf_vertex_major)."""
         import torch
+        self._need_full("vertex_major")
         if self._xv is None:
             M, V = self.member_count, self.node_count
             Xv = torch.empty((V, M), dtype=torch.float32, device=self.device)
@@ -179,8 +211,8 @@ class DeviceEnsemble:
         B = int(pos.shape[0])
         out = torch.empty((B, self.member_count), dtype=torch.float64, device=self.device)
         d = self.domain
-        N.call("ndf_sample_many", N.ptr(self.X), self.member_count, d.nx, d.ny, d.nz, N.ptr(pos), B,
-               N.ptr(out), N.stream_handle(self.device))
+        N.call("ndf_sample_many_ld", N.ptr(self.X), self.member_count, self.ld, self.col0, d.nx,
+               d.ny, d.nz, N.ptr(pos), B, N.ptr(out), N.stream_handle(self.device))
         return out
 
 

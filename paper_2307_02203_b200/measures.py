@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .ensemble import DeviceEnsemble, EnsembleField, _device_view
 from .errors import (CorruptFileError, DegenerateSampleError, FormatError,
-                     ParameterError)
+                     ParameterError, ShapeError)
 
 log = logging.getLogger(__name__)
 
@@ -256,14 +256,17 @@ def _check_dims(dims):
 
 def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: str, var_nu: str,
                               ref, dims, v0: int = 0, v1: int | None = None,
-                              chunk: int = 65536):
+                              chunk: int = 65536, ref_vec=None):
     """Device-resident ground truth for vertices [v0, v1) of ``dims`` (float32 CUDA tensor).
 
     Node-aligned grids (dims == the ensemble domain) read the ensemble
-    directly: Pearson through the standardised-ensemble GEMV, KSG through the
-    per-node kernel.  Other grids sample trilinearly first (bit-identical to
-    sample_many) and run the row kernels on the samples.  Degenerate Pearson
-    entries are NaN here; ``ground_truth_field`` maps them to 0 with a warning.
+    directly: Pearson in one streaming pass over the member columns
+    (ndf_pearson_field), KSG through the per-node kernel.  Other grids sample
+    trilinearly first (bit-identical to sample_many) and run the row kernels on
+    the samples.  Degenerate Pearson entries are NaN here; ``ground_truth_field``
+    maps them to 0 with a warning.  ``field_obj`` may be a column window
+    (DeviceEnsemble.window) covering [v0, v1); ``ref_vec`` (fp64 CUDA, M) then
+    supplies the reference's member vector, e.g. broadcast from the rank holding it.
     """
     import torch
     dims = _check_dims(dims)
@@ -275,30 +278,24 @@ def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: st
     dev = dnu.device
     stream = N.stream_handle(dev)
     M = dnu.member_count
-    ref_vec = dmu.sample_many(ref.reshape(1, 3))[0].contiguous()      # fp64 (M,)
+    if ref_vec is None:
+        ref_vec = dmu.sample_many(ref.reshape(1, 3))[0].contiguous()  # fp64 (M,)
+    else:
+        ref_vec = ref_vec.to(device=dev, dtype=torch.float64).contiguous()
+        if ref_vec.shape != (M,):
+            raise ShapeError(f"ref_vec must have {M} members, got {tuple(ref_vec.shape)}")
     out = torch.empty(v1 - v0, dtype=torch.float32, device=dev)
     node_aligned = dims == dnu.domain.dims
+    if not node_aligned and not dnu.full:
+        raise ParameterError("a column window serves node-aligned fields only")
+    if node_aligned and v0 < v1 and not dnu.col0 <= v0 <= v1 <= dnu.col0 + dnu.ld:
+        raise ParameterError("vertex range outside the ensemble's column window")
     if measure.kind == "pearson":
-        rc = ref_vec - ref_vec.mean()
-        var_ref = float((rc * rc).sum().item())
-        ref_deg = 1 if var_ref == 0.0 else 0
         if node_aligned:
-            Z, norm = dnu.zscore()
-            ref32 = ref_vec.to(torch.float32)
-            if ref_deg:
-                zref = torch.zeros(M, dtype=torch.float32, device=dev)
-            elif bool((ref32.to(torch.float64) == ref_vec).all().item()):
-                # fp32-exact (node) reference: standardise it with the very kernel
-                # that built Z, so the reference's own column matches bit for bit
-                # and comes back as exactly 1.0 (measures.py:102-107).
-                zref = torch.empty(M, dtype=torch.float32, device=dev)
-                nref = torch.empty(1, dtype=torch.float32, device=dev)
-                N.call("ndf_zscore", N.ptr(ref32.contiguous()), M, 1, 0, 1, N.ptr(zref), N.ptr(nref),
-                       stream)
-            else:
-                zref = (rc / np.sqrt(var_ref)).to(torch.float32).contiguous()
-            N.call("ndf_pearson_gemv", N.ptr(Z), N.ptr(norm), M, V, N.ptr(zref),
-                   ref_deg, v0, v1, N.ptr(out), stream)
+            # one streaming read of the member columns, reference statistics on device
+            # (ndf_pearson_field); no standardised copy, no host round trip
+            N.call("ndf_pearson_field", N.ptr(dnu.X), M, dnu.ld, dnu.col0, N.ptr(ref_vec), v0, v1,
+                   N.ptr(out), stream)
         else:
             pos = grid_positions(dims)[v0:v1]
             buf = torch.empty(min(chunk, max(len(pos), 1)), dtype=torch.float64, device=dev)
@@ -315,8 +312,10 @@ def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: st
         status = torch.zeros(1, dtype=torch.int32, device=dev)
         psi_km = _KsgTables.psi_km(k, M)
         if node_aligned:
-            N.call("ndf_ksg_ref_nodes", N.ptr(dnu.X), M, V, N.ptr(ref_vec), v0, v1, k, N.ptr(jit),
-                   N.ptr(psi), psi_km, None, N.ptr(out), None, N.ptr(status), stream)
+            # columns of a window are addressed relative to its first column
+            N.call("ndf_ksg_ref_nodes", N.ptr(dnu.X), M, dnu.ld, N.ptr(ref_vec), v0 - dnu.col0,
+                   v1 - dnu.col0, k, N.ptr(jit), N.ptr(psi), psi_km, None, N.ptr(out), None,
+                   N.ptr(status), stream)
         else:
             pos = grid_positions(dims)[v0:v1]
             for s in range(0, len(pos), chunk):

@@ -509,9 +509,9 @@ class DeviceModel:
         import torch
         spec = model.spec
         self.device = device
-        self.grid_mu = torch.from_numpy(np.ascontiguousarray(model.grid_mu, np.float32)).to(device)
+        self.grid_mu = torch.from_numpy(np.array(model.grid_mu, dtype=np.float32, copy=True)).to(device)
         self.grid_nu = self.grid_mu if spec.shared else torch.from_numpy(
-            np.ascontiguousarray(model.grid_nu, np.float32)).to(device)
+            np.array(model.grid_nu, dtype=np.float32, copy=True)).to(device)
         def flat(ws, bs):
             return np.concatenate([np.concatenate([w.ravel(), b.ravel()])
                                    for w, b in zip(ws, bs)]).astype(np.float32)

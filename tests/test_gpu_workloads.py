@@ -86,20 +86,62 @@ def _port():
     return p
 
 
-def test_sharded_query_single_rank_nccl():
+def test_sharded_paths_single_rank_nccl():
+    """The four sharded paths through NCCL on one rank (the gloo world-2 tests cover the
+    bookkeeping; one GPU is all this run has): each equals its unsharded call bitwise,
+    the ground-truth field through the V-slice window + reference broadcast."""
     import torch.distributed as dist
-    from paper_2307_02203_b200.parallel import reconstruct_field_sharded
+    from paper_2307_02203_b200 import parallel as P
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(_port())
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
         w = W.CONFIGS[0]
-        model = W.build_model(w, seed=0, grid_init=1.0).with_precision("fp16")
-        got = reconstruct_field_sharded(model, w.ref_position(), ndf.ROLE_MU, w.dims)
-        want = ndf.reconstruct_field_device(model, w.ref_position(), ndf.ROLE_MU, w.dims)
-        assert torch.equal(got, want)
+        ref = w.ref_position()
+        for prec in ("bf16", "fp16"):
+            model = W.build_model(w, seed=0, grid_init=1.0).with_precision(prec)
+            got = P.reconstruct_field_sharded(model, ref, ndf.ROLE_MU, w.dims)
+            assert torch.equal(got, ndf.reconstruct_field_device(model, ref, ndf.ROLE_MU, w.dims))
+            refs = np.array([ref, (0.3, -0.2, 0.9), (-1.0, 1.0, 0.0)])
+            cube = P.reconstruct_multi_sharded(model, refs, ndf.ROLE_MU, w.dims)
+            assert torch.equal(cube, ndf.reconstruct_multi_device(model, refs, ndf.ROLE_MU, w.dims))
+        f = W.generate_host(w)
+        for meas in (ndf.CorrelationMeasure("pearson"), ndf.CorrelationMeasure("ksg_mi", ksg_k=4)):
+            for r in (ref, (0.123, -0.45, 0.77)):          # node and off-node references
+                got = P.ground_truth_field_sharded(f, meas, "v", "v", r, w.dims)
+                want = ndf.ground_truth_field_device(f, meas, "v", "v", r, w.dims)
+                assert torch.equal(got.nan_to_num(), want.nan_to_num()), (meas.kind, r)
+        pa, pb = W.pair_list(w, count=500, seed=2)
+        got = P.pair_estimators_sharded(f, "v", pa, pb, k=4)
+        want = ndf.pair_estimators_device(f, "v", pa, pb, k=4)
+        for name in ("pearson", "ksg_mi"):
+            assert torch.equal(got[name].nan_to_num(), want[name].nan_to_num()), name
     finally:
         dist.destroy_process_group()
+
+
+def test_column_window_matches_whole_variable():
+    """DeviceEnsemble.window (a rank's V-slice): Pearson / KSG over vertices of the
+    window equal the whole-variable results bitwise; sampling inside the window too."""
+    w = W.CONFIGS[0]
+    f = W.generate_host(w)
+    X = f.member_grids("v")
+    c0, c1 = 1000, 3900
+    win = ndf.DeviceEnsemble.window(X, c0, c1)
+    full = ndf.DeviceEnsemble.from_numpy(X)
+    ref = w.ref_position()
+    vec = full.sample_many(np.asarray(ref).reshape(1, 3))[0]
+    for meas in (ndf.CorrelationMeasure("pearson"), ndf.CorrelationMeasure("ksg_mi", ksg_k=3)):
+        got = ndf.ground_truth_field_device(win, meas, "v", "v", ref, w.dims, 1200, 3000, ref_vec=vec)
+        want = ndf.ground_truth_field_device(full, meas, "v", "v", ref, w.dims, 1200, 3000)
+        assert torch.equal(got, want), meas.kind
+    pos = ndf.grid_positions(w.dims)[[1500, 2222]] + 1e-3
+    assert torch.equal(win.sample_many(pos), full.sample_many(pos))
+    with pytest.raises(ndf.ParameterError):
+        ndf.ground_truth_field_device(win, ndf.CorrelationMeasure("pearson"), "v", "v", ref,
+                                      w.dims, 500, 3000, ref_vec=vec)
+    with pytest.raises(ndf.ParameterError):
+        win.zscore()
 
 
 def test_load_ensemble_device_streams_one_variable(tmp_path):
