@@ -344,7 +344,7 @@ query_x3_kernel(const TcArgs t) {
   float* dotx = reinterpret_cast<float*>(bars + 32);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = warp_uniform(tid >> 5);
   const int lane = tid & 31;
   const int wg = warp >> 2;
   const int wq = warp & 3;
@@ -412,7 +412,7 @@ query_x3_kernel(const TcArgs t) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // prep tables ready
   if (tid < kC) eref_s[tid] = t.erefs[tid];
   __syncthreads();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kHid >> 3) << 17) |
                          ((uint32_t)(kTileM >> 4) << 24);
 
@@ -458,29 +458,29 @@ query_x3_kernel(const TcArgs t) {
 #pragma unroll 1
           for (int k2 = 0; k2 < 4; ++k2) {
             if (!t.x3_burst) named_bar(1 + 4 * si + k2, 288);
-            if (lane == 0) {
-              tc_fence_after();
-              if (k2 == 0)
-                mma_bf16(d_next, smem_desc(smem_u32(bias_s), (uint32_t)(H * kX3Blk), 128),
-                         smem_desc(smem_u32(bias_s) + (uint32_t)((l + 1) * kX3Blk),
-                                   (uint32_t)((H - l - 1) * kX3Blk), 128),
-                         idesc, 0u);
+            // the whole issuer warp runs this (elect.sync inside the MMA asm): operands
+            // stay in uniform registers, MMAs go out back to back
+            tc_fence_after();
+            if (k2 == 0)
+              mma_ss_warp(d_next, smem_desc(smem_u32(bias_s), (uint32_t)(H * kX3Blk), 128),
+                          smem_desc(smem_u32(bias_s) + (uint32_t)((l + 1) * kX3Blk),
+                                    (uint32_t)((H - l - 1) * kX3Blk), 128),
+                          idesc, 0u);
 #pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const int ks = 2 * k2 + j;
-                const uint64_t bh = smem_desc(whi + ks * 256, 128, kSboA);
-                mma_ts(d_next, a_tm + (uint32_t)(16 * ks), bh, idesc, 1u);
+            for (int j = 0; j < 2; ++j) {
+              const int ks = 2 * k2 + j;
+              const uint64_t bh = smem_desc(whi + ks * 256, 128, kSboA);
+              mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks), bh, idesc, 1u);
 #ifndef NDF_EXP_X3_ONEMMA    // timing experiment: hi x hi only (wrong results)
-                mma_ts(d_next, a_tm + (uint32_t)(16 * ks + 8), bh, idesc, 1u);
-                if (use_lo) mma_ts(d_next, a_tm + (uint32_t)(16 * ks),
-                                   smem_desc(wlo + ks * 256, 128, kSboA), idesc, 1u);
+              mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks + 8), bh, idesc, 1u);
+              if (use_lo) mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks),
+                                      smem_desc(wlo + ks * 256, 128, kSboA), idesc, 1u);
 #else
-                (void)use_lo; (void)wlo;
+              (void)use_lo; (void)wlo;
 #endif
-              }
-              if (k2 == 3) mma_commit(&acc_full[si]);
-              NDF_X3_TRACE(si, (int)kk, 12 + 4 * l + k2);
             }
+            if (k2 == 3) mma_commit_warp(&acc_full[si]);
+            if (lane == 0) NDF_X3_TRACE(si, (int)kk, 12 + 4 * l + k2);
           }
         }
       }
@@ -534,27 +534,27 @@ query_x3_kernel(const TcArgs t) {
                      pv[4 * g + 2], pv[4 * g + 3]);
       fence_proxy_async();
       named_bar(11 + s, 128);
-      if (wtid == 0) {
+      if (wq == 0) {                 // the producer's first warp issues layer 0 (elect.sync)
         if (kk == 0) mbar_wait(wbar, 0);
         else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
-        NDF_X3_TRACE(s, (int)kk, 3);
+        if (lane == 0) NDF_X3_TRACE(s, (int)kk, 3);
         mbar_wait(&b_full[s], (uint32_t)(kk & 1));
         tc_fence_after();
         const uint32_t d0 = d_slot + (uint32_t)((kk * H) & 1) * kHid;
-        mma_bf16(d0, smem_desc(smem_u32(selx), 128, 256), smem_desc(bx_a, 2048, 128), idesc, 0u);
-        mma_bf16(d0, smem_desc(smem_u32(selyz), 128, 512), smem_desc(byz_a, 2048, 128), idesc, 1u);
-        mma_bf16(d0, smem_desc(smem_u32(selyz) + 256, 128, 512), smem_desc(byz_a + 4096, 2048, 128),
-                 idesc, 1u);
+        mma_ss_warp(d0, smem_desc(smem_u32(selx), 128, 256), smem_desc(bx_a, 2048, 128), idesc, 0u);
+        mma_ss_warp(d0, smem_desc(smem_u32(selyz), 128, 512), smem_desc(byz_a, 2048, 128), idesc, 1u);
+        mma_ss_warp(d0, smem_desc(smem_u32(selyz) + 256, 128, 512),
+                    smem_desc(byz_a + 4096, 2048, 128), idesc, 1u);
 #pragma unroll
         for (int st = 0; st < 2; ++st) {
           const uint64_t bh = smem_desc(wlat_hi + st * 256, 128, 512);
-          mma_bf16(d0, smem_desc(alat_a + st * 256, 128, 1024), bh, idesc, 1u);         // hi x hi
-          mma_bf16(d0, smem_desc(alat_a + (2 + st) * 256, 128, 1024), bh, idesc, 1u);   // lo x hi
-          mma_bf16(d0, smem_desc(alat_a + st * 256, 128, 1024),
-                   smem_desc(wlat_lo + st * 256, 128, 512), idesc, 1u);                 // hi x lo
+          mma_ss_warp(d0, smem_desc(alat_a + st * 256, 128, 1024), bh, idesc, 1u);         // hi x hi
+          mma_ss_warp(d0, smem_desc(alat_a + (2 + st) * 256, 128, 1024), bh, idesc, 1u);   // lo x hi
+          mma_ss_warp(d0, smem_desc(alat_a + st * 256, 128, 1024),
+                      smem_desc(wlat_lo + st * 256, 128, 512), idesc, 1u);                 // hi x lo
         }
-        mma_commit(&acc_full[s]);
-        NDF_X3_TRACE(s, (int)kk, 4);
+        mma_commit_warp(&acc_full[s]);
+        if (lane == 0) NDF_X3_TRACE(s, (int)kk, 4);
       }
     }
   } else {
@@ -584,6 +584,14 @@ query_x3_kernel(const TcArgs t) {
         tmem_ld16_nowait(d_base + first_col, va);
         tmem_wait_ld();
         if (l + 1 < H) {
+#ifdef NDF_EXP_X3_NOEPI      // timing experiment: hidden epilogues only signal (wrong results)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            tc_fence_before();
+            named_bar_arrive(1 + 4 * s + i, 288);
+          }
+          (void)vb;
+#else
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t col = first_col + 32u * (uint32_t)i;
@@ -596,6 +604,7 @@ query_x3_kernel(const TcArgs t) {
             named_bar_arrive(1 + 4 * s + i, 288);
             if (i + 1 < 4) tmem_wait_ld();
           }
+#endif
           if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
         } else {
           if (lead && lane == 0) mbar_arrive(&d_free[s]);

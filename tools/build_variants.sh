@@ -7,7 +7,7 @@ set -e
 cd "$(dirname "$0")/.."
 python -m paper_2307_02203_b200.build > /dev/null
 mkdir -p variants
-OBJS="build/obj/ndf_capi.o build/obj/ndf_ksg.o build/obj/ndf_pearson.o build/obj/ndf_query_f32.o"
+OBJS=$(ls build/obj/*.o | grep -v ndf_query_tc.o)
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -I paper_2307_02203_b200/csrc"
 for v in "$@"; do
   case $v in
