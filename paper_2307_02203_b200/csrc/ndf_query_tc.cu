@@ -876,9 +876,21 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
 // SiLU of 16 pre-halved accumulators: h = y + y tanh(y) (weights and biases of SiLU
 // layers are pre-scaled by 1/2), one MUFU tanh per element and packed fp32 FMAs
 // (fma.rn.f32x2: same rounding as fmaf, half the issue slots).
+// NDF_POLY_PAIRS pairs of the 16 (the last 2 * NDF_POLY_PAIRS columns of every sub-chunk)
+// take tanh from tanh2_fma on the FMA pipe instead of MUFU (ndf_tc_ptx.cuh).  Measured on
+// B200 and rejected (default 0): 1 / 2 / 3 pairs cost bf16 0.327 -> 0.352 / 0.361 / 0.395 ms
+// and fp16 0.241 -> 0.250 / 0.287 / 0.308 ms -- the epilogue is bound by instruction issue
+// and latency, not by MUFU throughput, so ~15 extra instructions per pair lose more than
+// the freed MUFU slots gain.
+#ifndef NDF_POLY_PAIRS
+#define NDF_POLY_PAIRS 0
+#endif
 __device__ __forceinline__ void silu16(const float* x, float* h) {
+  constexpr int kMufu = 16 - 2 * NDF_POLY_PAIRS;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) h[i] = NDF_EXP_TANH(x[i]);
+  for (int i = 0; i < kMufu; ++i) h[i] = NDF_EXP_TANH(x[i]);
+#pragma unroll
+  for (int i = kMufu; i < 16; i += 2) tanh2_fma(x[i], x[i + 1], h[i], h[i + 1]);
 #pragma unroll
   for (int i = 0; i < 16; i += 2)
     ffma2(h[i], h[i + 1], x[i], x[i + 1], h[i], h[i + 1], x[i], x[i + 1]);

@@ -168,6 +168,63 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
+// Packed fp32 add / mul (sm_100a FADD2 / FMUL2).
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// tanh of a pair on the FMA / integer pipes, no MUFU:
+//   tanh|y| = 1 - 2 / (1 + 2^z),  z = 2 |y| log2(e) clamped to 64,
+//   2^z = 2^n * p(f) (n = round(z) by the 1.5 * 2^23 trick, f in [-0.5, 0.5], p a degree-5
+//   fit, 2.3e-7 relative in fp32 Horner), the reciprocal by a bit-trick seed and three
+//   Newton steps (~4e-8); sign restored.  |error| <= ~3e-7, below what SiLU's fp32 output
+//   resolves; NaN in -> NaN out through the caller's y + y * t.  Lets part of the epilogue's
+//   tanh leave the (binding) MUFU pipe for the FMA pipe, which the epilogue leaves mostly idle.
+__device__ __forceinline__ void tanh2_fma(float y0, float y1, float& t0, float& t1) {
+  const float kM = 12582912.0f;   // 1.5 * 2^23: z + kM rounds z to an integer in the low bits
+  float z0, z1;
+  fmul2(z0, z1, fabsf(y0), fabsf(y1), 2.8853900817779268f, 2.8853900817779268f);
+  z0 = fminf(z0, 64.0f);
+  z1 = fminf(z1, 64.0f);
+  float m0, m1, n0, n1, f0, f1;
+  fadd2(m0, m1, z0, z1, kM, kM);
+  fadd2(n0, n1, m0, m1, -kM, -kM);
+  ffma2(f0, f1, n0, n1, -1.0f, -1.0f, z0, z1);                       // f = z - n
+  float p0 = 0.0013267219765111804f, p1 = 0.0013267219765111804f;
+  ffma2(p0, p1, p0, p1, f0, f1, 0.009675461798906326f, 0.009675461798906326f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.055507417768239975f, 0.055507417768239975f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.24022121727466583f, 0.24022121727466583f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.6931469440460205f, 0.6931469440460205f);
+  ffma2(p0, p1, p0, p1, f0, f1, 1.0000001192092896f, 1.0000001192092896f);
+  const int kMb = 0x4B400000;      // bits of kM
+  const float e0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(m0) - kMb) << 23));
+  const float e1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(m1) - kMb) << 23));
+  float d0, d1;
+  fadd2(d0, d1, e0, e1, 1.0f, 1.0f);
+  float r0 = __int_as_float(0x7EF311C7 - __float_as_int(d0));
+  float r1 = __int_as_float(0x7EF311C7 - __float_as_int(d1));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    float q0, q1;
+    ffma2(q0, q1, -d0, -d1, r0, r1, 1.0f, 1.0f);
+    ffma2(r0, r1, r0, r1, q0, q1, r0, r1);
+  }
+  ffma2(t0, t1, -2.0f, -2.0f, r0, r1, 1.0f, 1.0f);
+  t0 = __int_as_float(__float_as_int(t0) | (__float_as_int(y0) & 0x80000000));
+  t1 = __int_as_float(__float_as_int(t1) | (__float_as_int(y1) & 0x80000000));
+}
+
 template <bool F16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   if constexpr (F16) {

@@ -1,4 +1,4 @@
-"""Config-3 probe: 64-reference fp16 cube for both heads (timing only)."""
+"""Config-3 probe: 64-reference fp16 cube for both heads, PREC=bf16|fp16 MLP (timing only)."""
 import os
 import sys
 
@@ -15,9 +15,10 @@ refs = W.reference_vertices(w3, count=64, seed=1)
 pos = np.stack([np.array([2.0 * i / (n - 1) - 1.0 for i, n in
                           zip((v % w3.dims[0], (v // w3.dims[0]) % w3.dims[1],
                                v // (w3.dims[0] * w3.dims[1])), w3.dims)]) for v in refs])
-models = [W.build_model(w3, seed=0, grid_init=1e-4).with_precision("fp16"),
+PREC = os.environ.get("PREC", "bf16")
+models = [W.build_model(w3, seed=0, grid_init=1e-4).with_precision(PREC),
           ndf.NdfModel.build(ndf.ModelSpec.baseline(w3.dims, w3.latent_factor, measure_kind="ksg_mi",
-                                                    precision="fp16"), seed=1)]
+                                                    precision=PREC), seed=1)]
 cube = torch.empty((64, V), dtype=torch.float16, device="cuda")
 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ts = []

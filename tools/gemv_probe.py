@@ -1,4 +1,4 @@
-"""Pearson GEMV over the z-scored config-1 ensemble (profiling probe)."""
+"""Ground-truth Pearson field on config 1 (the public path: ndf_pearson_field; profiling probe)."""
 import os
 import sys
 
