@@ -334,7 +334,7 @@ def run_reference(args):
 
 # x3 (bf16 split operands) issues per 128-row tile: layer 0 = 3 selector + 6 latent K16
 # MMAs, each hidden layer = bias + 3 x 8 K16 MMAs (A_hi W_hi, A_lo W_hi, A_hi W_lo);
-# tiles are 8 x 16 nodes (ceil(250/8) x ceil(7040/16) tiles at config 1)
+# tiles are 16 x 8 nodes (ceil(250/16) x ceil(7040/8) tiles at config 1)
 X3_MMAS_PER_TILE = 9 + 2 * 25
 MMA_FLOP = 2 * 128 * 128 * 16
 
@@ -342,7 +342,7 @@ MMA_FLOP = 2 * 128 * 128 * 16
 def issued_tensor_flop(precision, dims):
     nx, ny, nz = dims
     if precision == "bf16":
-        tiles = math.ceil(nx / 8) * math.ceil(ny * nz / 16)
+        tiles = math.ceil(nx / 16) * math.ceil(ny * nz / 8)
         return tiles * X3_MMAS_PER_TILE * MMA_FLOP
     tiles = math.ceil(nx * ny * nz / 128)
     return tiles * (8 + 2 * 9) * MMA_FLOP          # fp16 ping-pong: bias + 7, bias + 8 (x2)
@@ -473,7 +473,7 @@ def run_ours(args):
             if args.precision == "bf16":
                 roof["issued_note"] = ("split operands: each hidden K16 step runs A_hi W_hi + "
                                        "A_lo W_hi + A_hi W_lo; layer 0 is 3 selector + 6 latent "
-                                       "MMAs; 8x16-node tiles")
+                                       "MMAs; 16x8-node tiles")
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,

@@ -9,12 +9,27 @@
 //
 // Layout: one thread per point; the E features of the block's 128 points are staged in
 // SMEM ([point][E + 1], odd stride against bank conflicts) and written back as one
-// contiguous (128 x E) fp32 slab, so the stores are coalesced.
+// contiguous (128 x E) fp32 slab, so the stores are coalesced.  Grid nodes of dense-latent
+// models take the separable per-axis route (embed_nodes_kernel below).
 #include "ndf_query.cuh"
 
 namespace ndf {
 
 constexpr int kEmbThreads = 128;
+
+// Coalesced store of the block's staged (rows x E) slab (SMEM row stride ld): flat
+// element k = r * E + c; the row index comes from one float multiply (exact here:
+// k < 128 * 140, so (k + 0.5) / E never lies within float error of an integer) instead
+// of an integer division per element.
+__device__ __forceinline__ void store_slab(const float* stage, int ld, int E, int rows,
+                                           float* __restrict__ dst) {
+  const float invE = 1.0f / (float)E;
+  const int total = rows * E;
+  for (int k = threadIdx.x; k < total; k += kEmbThreads) {
+    const int r = (int)(((float)k + 0.5f) * invE);
+    dst[k] = stage[r * ld + (k - r * E)];
+  }
+}
 
 // mode 0: grid nodes [v0, v0 + n) of an nx x ny x nz output grid (x fastest,
 // node_coord positions, measures.py:240-252); mode 1: fp64 points pos[3 i ..].
@@ -49,12 +64,124 @@ embed_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int mode, in
     embed_point(g, grid, p[0], p[1], p[2], [&](int k, float x) { row[k] = x; });
   }
   __syncthreads();
-  const int64_t rows = min((int64_t)kEmbThreads, n - base);
-  float* dst = out + base * E;
-  for (int64_t k = threadIdx.x; k < rows * E; k += kEmbThreads) {
-    const int r = (int)(k / E), c = (int)(k - (int64_t)r * E);
-    dst[k] = stage[r * ld + c];
+  store_slab(stage, ld, E, (int)min((int64_t)kEmbThreads, n - base), out + base * E);
+}
+
+// ---- grid nodes of a dense-latent model: separable per axis ----------------------
+// Every feature of a grid node except the latent channels depends on ONE axis node
+// (raw p, Fourier sin / cos), and so do the latent cell (i0, t) per axis: an axis table
+// computed once per launch (one fp64 sincos per node x octave, the same operations as
+// embed_point -> the same bits) turns the node embedding into table reads plus the fp64
+// eight-corner latent sum -- so the launch is bound by writing the (V, E) output.
+constexpr int kAxisRowF = 32;       // [p | sin, cos x L (L <= 12) | pad | t (fp64) | i0]
+
+__global__ void embed_axis_kernel(const EmbedGeom g, int nx, int ny, int nz, float* __restrict__ tab) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nodes = nx + ny + nz;
+  const int L = g.L;
+  if (item >= nodes * (L + 1)) return;
+  const int node = item / (L + 1), o = item % (L + 1);
+  int i, n, res;
+  if (node < nx) { i = node; n = nx; res = g.rx; }
+  else if (node < nx + ny) { i = node - nx; n = ny; res = g.ry; }
+  else { i = node - nx - ny; n = nz; res = g.rz; }
+  const double p = fmin(fmax(node_coord(i, n), -1.0), 1.0);
+  float* row = tab + (size_t)node * kAxisRowF;
+  if (o == L) {                       // raw coordinate and the latent cell of this axis
+    row[0] = (float)p;
+    const AxisCoord c = level_coord(p, res);
+    reinterpret_cast<double*>(row)[14] = c.t;      // floats 28-29
+    reinterpret_cast<int*>(row)[30] = c.i0;
+    return;
   }
+  double scale = 3.141592653589793;
+  for (int k = 0; k < o; ++k) scale = scale * 2.0;
+  double sn, cs;
+  sincos(dmul(scale, p), &sn, &cs);
+  row[1 + 2 * o] = (float)sn;
+  row[2 + 2 * o] = (float)cs;
+}
+
+__global__ void __launch_bounds__(kEmbThreads)
+embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx, int ny, int nz,
+                   int64_t v0, int64_t n, const float* __restrict__ tab, float* __restrict__ out) {
+  extern __shared__ float stage[];
+  const int E = g.E, L = g.L, C = g.C;
+  const int ld = E + 1;
+  const float* grid = branch == 0 ? m.grid_mu : m.grid_nu;
+  const int64_t base = (int64_t)blockIdx.x * kEmbThreads;
+  const int64_t i = base + threadIdx.x;
+  if (i < n) {
+    const int64_t v = v0 + i;
+    const int64_t plane = (int64_t)nx * ny;
+    const int iz = (int)(v / plane);
+    const int64_t r = v - (int64_t)iz * plane;
+    const int iy = (int)(r / nx);
+    const int ix = (int)(r - (int64_t)iy * nx);
+    const float* rows[3] = {tab + (size_t)ix * kAxisRowF, tab + (size_t)(nx + iy) * kAxisRowF,
+                            tab + (size_t)(nx + ny + iz) * kAxisRowF};
+    float* dst = stage + threadIdx.x * ld;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) dst[ax] = __ldg(rows[ax]);
+    for (int o = 0; o < L; ++o) {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        dst[3 + 6 * o + 2 * ax] = __ldg(rows[ax] + 1 + 2 * o);
+        dst[3 + 6 * o + 2 * ax + 1] = __ldg(rows[ax] + 2 + 2 * o);
+      }
+    }
+    // latent: embed_point's corner order, weights ((wx) * wy) * wz and fp64 sums
+    double tt[3];
+    int i0[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      tt[ax] = __ldg(reinterpret_cast<const double*>(rows[ax]) + 14);
+      i0[ax] = __ldg(reinterpret_cast<const int*>(rows[ax]) + 30);
+    }
+    double w[8];
+    int idx[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+      const double wx = dx ? tt[0] : dsub(1.0, tt[0]);
+      const double wy = dy ? tt[1] : dsub(1.0, tt[1]);
+      const double wz = dz ? tt[2] : dsub(1.0, tt[2]);
+      w[c] = dmul(dmul(wx, wy), wz);
+      idx[c] = (i0[0] + dx) + g.rx * ((i0[1] + dy) + g.ry * (i0[2] + dz));
+    }
+    const int lb = 3 + 6 * L;
+    if (C == 16) {
+      // corner-outer with 16-byte loads; per channel the corner order (and so the
+      // fp64 rounding sequence) is embed_point's
+      double acc[16];
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) acc[ch] = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4* rowp = reinterpret_cast<const float4*>(grid + (size_t)idx[c] * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 f = __ldg(rowp + q);
+          acc[4 * q + 0] = dadd(acc[4 * q + 0], dmul(w[c], (double)f.x));
+          acc[4 * q + 1] = dadd(acc[4 * q + 1], dmul(w[c], (double)f.y));
+          acc[4 * q + 2] = dadd(acc[4 * q + 2], dmul(w[c], (double)f.z));
+          acc[4 * q + 3] = dadd(acc[4 * q + 3], dmul(w[c], (double)f.w));
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) dst[lb + ch] = (float)acc[ch];
+    } else {
+      for (int ch = 0; ch < C; ++ch) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          acc = dadd(acc, dmul(w[c], (double)__ldg(grid + (size_t)idx[c] * C + ch)));
+        dst[lb + ch] = (float)acc;
+      }
+    }
+  }
+  __syncthreads();
+  store_slab(stage, ld, E, (int)min((int64_t)kEmbThreads, n - base), out + base * E);
 }
 
 static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int nx, int ny, int nz,
@@ -69,6 +196,32 @@ static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int n
   if ((st = resolve_output(out, &out_dev))) return st;
   const EmbedGeom g = make_geom(*m);
   const size_t smem = (size_t)kEmbThreads * (g.E + 1) * sizeof(float);
+  if (mode == 0 && g.levels == 0) {
+    // dense-latent model over grid nodes: per-axis tables, then table reads + latent sum
+    static SmemAttrCache attr_n;
+    NDF_CUDA_CHECK(attr_n.ensure(embed_nodes_kernel,
+                                 (size_t)kEmbThreads * (kMaxEmbed + 1) * sizeof(float)));
+    const int nodes = nx + ny + nz;
+    void* tab = nullptr;
+    NDF_CUDA_CHECK(scratch_alloc(&tab, (size_t)nodes * kAxisRowF * sizeof(float),
+                                 as_stream(stream)));
+    const int items = nodes * (g.L + 1);
+    embed_axis_kernel<<<(items + 127) / 128, 128, 0, as_stream(stream)>>>(g, nx, ny, nz,
+                                                                          static_cast<float*>(tab));
+    cudaError_t e = cudaGetLastError();
+    count_launch();
+    if (e == cudaSuccess) {
+      embed_nodes_kernel<<<(unsigned)((n + kEmbThreads - 1) / kEmbThreads), kEmbThreads, smem,
+                           as_stream(stream)>>>(*m, g, branch, nx, ny, nz, v0, n,
+                                                static_cast<const float*>(tab),
+                                                static_cast<float*>(out_dev));
+      e = cudaGetLastError();
+      count_launch();
+    }
+    cudaFreeAsync(tab, as_stream(stream));
+    NDF_CUDA_CHECK(e);
+    return NDF_OK;
+  }
   static SmemAttrCache attr;
   NDF_CUDA_CHECK(attr.ensure(embed_kernel, (size_t)kEmbThreads * (kMaxEmbed + 1) * sizeof(float)));
   embed_kernel<<<(unsigned)((n + kEmbThreads - 1) / kEmbThreads), kEmbThreads, smem,

@@ -1081,7 +1081,10 @@ query_pp_kernel(const TcArgs t) {
 
   if (wg == 6) {
     // ======================== MMA issuer of slot warp - 24 ===========================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+#ifndef NDF_PP_ISSUER_REGS
+#define NDF_PP_ISSUER_REGS 24
+#endif
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(NDF_PP_ISSUER_REGS));
     const int si = warp - 24;
     if (si < kPPSlots) {
       const int64_t fi = (int64_t)blockIdx.x * kPPSlots + si;
@@ -1102,6 +1105,16 @@ query_pp_kernel(const TcArgs t) {
             NDF_TRACE_WARP(2 * k2);
             // whole issuer warp (elect.sync inside the MMA asm): uniform operands, the
             // MMAs go out back to back (x3 kernel: 0.41 -> 0.33 ms from this alone)
+#ifdef NDF_PP_LANE0_ISSUER   // A/B: round-1 single-lane issue
+            if (lane == 0) {
+              tc_fence_after();
+              if (k2 == 0)
+                mma_bf16(d_next, smem_desc(smem_u32(ones_blk), 128, 256),
+                         smem_desc(smem_u32(bias_blk + (l + 1) * kBiasBlk), 128, 256), idesc, 0u);
+              issue_ksteps_ts(d_next, a_tm, wl, 2 * k2, 2, kSboA, idesc, true);
+              if (k2 == 3) mma_commit(&acc_full[si]);
+            }
+#else
             tc_fence_after();
             if (k2 == 0)
               mma_ss_warp(d_next, smem_desc(smem_u32(ones_blk), 128, 256),      // D = bias
@@ -1112,6 +1125,7 @@ query_pp_kernel(const TcArgs t) {
             (void)a_tm; (void)wl;
 #endif
             if (k2 == 3) mma_commit_warp(&acc_full[si]);
+#endif
             NDF_TRACE_WARP(2 * k2 + 1);
           }
         }
@@ -1182,6 +1196,23 @@ query_pp_kernel(const TcArgs t) {
       cp_async_wait_all();
       fence_proxy_async();
       named_bar(11 + s, 128);
+#ifndef NDF_PP_WARP_PRODUCER
+      // Layer 0 is issued by one producer thread.  A warp-collective producer issue (as
+      // the issuer warps and the x3 kernel use) deadlocked this kernel within 50-800
+      // back-to-back c1 queries on B200 (tools/stress_query.py; either change alone
+      // passes 6,000 + 20,000, as does the x3 kernel with both: 35,000) -- root cause not
+      // found, so the single-thread form stays here (it costs 0.006 ms).
+      if (wtid == 0) {
+        if (kk == 0) mbar_wait(wbar, 0);
+        else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));
+        tc_fence_after();
+        const uint32_t half = (uint32_t)((kk * H) & 1);
+        mma_bf16(d_slot + half * kHid, smem_desc(smem_u32(ones_blk), 128, 256),
+                 smem_desc(smem_u32(bias_blk), 128, 256), idesc, 0u);
+        issue_ksteps(d_slot + half * kHid, a_addr, w_addr, 0, lay.kin / 16, sbo_w0, idesc, true);
+        mma_commit(&acc_full[s]);
+      }
+#else
       if (wq == 0) {                  // the producer's first warp issues layer 0 (elect.sync)
         if (kk == 0) mbar_wait(wbar, 0);
         else mbar_wait(&d_free[s], (uint32_t)((kk - 1) & 1));   // target D half drained
@@ -1193,6 +1224,7 @@ query_pp_kernel(const TcArgs t) {
                           true);
         mma_commit_warp(&acc_full[s]);
       }
+#endif
       NDF_TRACE_AT((int)kk, 3);
     }
   } else {
@@ -1671,9 +1703,9 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
   }
   t.x3_burst = burst;
   const int nnode = a.nx + a.ny + a.nz + 3 * n_ref;
-  const int ngx = (a.nx + tc::kX3TX - 1) / tc::kX3TX * 2;
+  const int ngx = (a.nx + tc::kX3TX - 1) / tc::kX3TX * (tc::kX3TX / 4);
   const tc::X3Tiles tg = tc::x3_tiles(a.nx, a.v0, a.v1);
-  const int64_t ngyz64 = tg.n_vt / (tg.n_xt) * 4;        // row-tiles of this launch x 4 groups
+  const int64_t ngyz64 = tg.n_vt / (tg.n_xt) * (tc::kX3TY / 4);   // this launch's row-tiles
   NDF_REQUIRE(ngyz64 < (1LL << 30), NDF_ERR_UNSUPPORTED, "too many (y, z) rows for the bf16 path");
   const int ngyz = (int)ngyz64;
   NDF_REQUIRE((int64_t)n_ref * (ngx + ngyz) < (1LL << 31), NDF_ERR_UNSUPPORTED,

@@ -13,11 +13,11 @@
 //       z0 = PX[ix] + PYZ[iy, iz] + W_lat^T [r + lat, |r - lat|]
 //   with PX / PYZ (bias folded into PYZ) computed per query in fp64 by
 //   prep_x3_tab_kernel from the fp32 merged features and fp32 weights, stored as
-//   bf16 hi + lo pairs (16 significant bits).  A tile is 8 x-nodes x 16 (y, z)-rows,
+//   bf16 hi + lo pairs (16 significant bits).  A tile is 16 x-nodes x 8 (y, z)-rows,
 //   so PX and PYZ enter the accumulator through two constant one-hot selector blocks
-//   (A = [1 1] in the columns of the row's node, B = the tile's 8 PX / 16 PYZ rows,
+//   (A = [1 1] in the columns of the row's node, B = the tile's 16 PX / 8 PYZ rows,
 //   hi and lo): 3 K16 MMA steps, and each tile's B blocks are two contiguous bulk
-//   copies (4 KB + 8 KB) from the tables (LBO = 2048 B along K, SBO = 128 B along N).
+//   copies (8 KB + 4 KB) from the tables (LBO = 2048 B along K, SBO = 128 B along N).
 //   The latent words go hi/lo as well: A_hi W_hi + A_lo W_hi + A_hi W_lo (6 steps).
 // * Hidden layers: the epilogue writes each 16-column sub-chunk's activations as 8 hi
 //   words + 8 lo words (h - bf16(h) is exact in fp32) into the sub-chunk's own 16
@@ -33,13 +33,20 @@
 // producer now only builds the 32 latent words, issues the two bulk copies and the 9
 // layer-0 MMAs; the issuer sends 3 MMAs per K16 step.
 
-constexpr int kX3TX = 8;                  // tile: 8 x-nodes ...
-constexpr int kX3TY = 16;                 // ... x 16 (y, z)-rows = 128 rows
+// Tile = kX3TX x-nodes x kX3TY (y, z)-rows = 128 rows (row m: x offset m % TX, row
+// offset m / TX).  16 x 8: the tile's outputs are 8 runs of 16 consecutive vertices
+// (64 B stores -- the field goes straight to pinned host memory over PCIe, where 8 x 16
+// tiles' 32 B runs measured slower end to end), and the selectors still take 3 K16 MMAs.
+constexpr int kX3TX = 16;
+constexpr int kX3TY = 8;
+static_assert(kX3TX * kX3TY == 128 && kX3TX % 8 == 0 && kX3TY % 8 == 0, "x3 tile shape");
 constexpr int kX3Blk = 128 * 16;          // one 8-K group of a 128-row operand (2 KB)
-constexpr int kX3SelX = 2 * kX3Blk;       // A selector for PX (K = 16)
-constexpr int kX3SelYZ = 4 * kX3Blk;      // A selector for PYZ (K = 32)
-constexpr int kX3Bx = 2 * kX3Blk;         // per slot: B = 8 PX rows (hi, lo)
-constexpr int kX3Byz = 4 * kX3Blk;        // per slot: B = 16 PYZ rows (hi, lo)
+constexpr int kX3KX = 2 * kX3TX;          // selector K for PX: (node, hi/lo)
+constexpr int kX3KYZ = 2 * kX3TY;         // selector K for PYZ
+constexpr int kX3SelX = (kX3KX / 8) * kX3Blk;     // A selector for PX
+constexpr int kX3SelYZ = (kX3KYZ / 8) * kX3Blk;   // A selector for PYZ
+constexpr int kX3Bx = (kX3KX / 8) * kX3Blk;       // per slot: B = the tile's PX rows (hi, lo)
+constexpr int kX3Byz = (kX3KYZ / 8) * kX3Blk;     // per slot: B = the tile's PYZ rows
 constexpr int kX3ALat = 8 * kX3Blk;       // per slot: latent A, hi words K 0-31, lo 32-63
 constexpr int kX3Slot = kX3Bx + kX3Byz + kX3ALat;
 constexpr int kX3Lat = 3 + 6 * kL;        // first latent feature (39)
@@ -293,7 +300,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
 }
 
 // Tile geometry of a launch over flat vertices [v0, v1) of an nx x ny x nz grid: tiles of
-// 8 x-nodes x 16 (y, z)-rows covering rows v0 / nx .. (v1 - 1) / nx; rows and nodes
+// kX3TX x-nodes x kX3TY (y, z)-rows covering rows v0 / nx .. (v1 - 1) / nx; rows and nodes
 // outside the range are computed and discarded.
 struct X3Tiles {
   int n_xt;          // tiles along x
@@ -386,14 +393,15 @@ query_x3_kernel(const TcArgs t) {
       }
       st_shared_v4(smem_u32(bias_s + blk * kX3Blk) + r * 16, w0, 0u, 0u, 0u);
     }
-    for (int i = tid; i < 128 * 6; i += blockDim.x) {
-      const int r = i % 128, g = i / 128;          // g 0-1: selx K-group, 2-5: selyz K-group
+    constexpr int gx = kX3KX / 8, gyz = kX3KYZ / 8;     // 8-K groups of each selector
+    for (int i = tid; i < 128 * (gx + gyz); i += blockDim.x) {
+      const int r = i % 128, g = i / 128;
       uint32_t w[4];
-      const int hot = g < 2 ? (r & 7) - 4 * g : (r >> 3) - 4 * (g - 2);
+      const int hot = g < gx ? (r % kX3TX) - 4 * g : (r / kX3TX) - 4 * (g - gx);
 #pragma unroll
       for (int u = 0; u < 4; ++u) w[u] = (u == hot) ? kBf16One2 : 0u;
-      const uint32_t addr = g < 2 ? smem_u32(selx) + canon_off(r, 8 * g, 256)
-                                  : smem_u32(selyz) + canon_off(r, 8 * (g - 2), 512);
+      const uint32_t addr = g < gx ? smem_u32(selx) + canon_off(r, 8 * g, gx * 128)
+                                   : smem_u32(selyz) + canon_off(r, 8 * (g - gx), gyz * 128);
       st_shared_v4(addr, w[0], w[1], w[2], w[3]);
     }
     fence_proxy_async();
@@ -491,7 +499,7 @@ query_x3_kernel(const TcArgs t) {
     uint8_t* slot = slots + s * kX3Slot;
     const uint32_t bx_a = smem_u32(slot), byz_a = bx_a + kX3Bx, alat_a = byz_a + kX3Byz;
     const uint32_t wlat_hi = smem_u32(ext_s) + xl.wlat_hi, wlat_lo = smem_u32(ext_s) + xl.wlat_lo;
-    const int j = wtid & 7, q = wtid >> 3;
+    const int j = wtid % kX3TX, q = wtid / kX3TX;
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
       int r, tx, ty;
@@ -523,9 +531,11 @@ query_x3_kernel(const TcArgs t) {
         NDF_X3_TRACE(s, (int)kk, 2);
         mbar_expect_tx(&b_full[s], (uint32_t)(kX3Bx + kX3Byz));
         bulk_g2s(slot, reinterpret_cast<const uint8_t*>(t.px) +
-                           ((size_t)r * t.ngx + 2 * tx) * (size_t)kX3Blk, kX3Bx, &b_full[s]);
+                           ((size_t)r * t.ngx + (kX3TX / 4) * tx) * (size_t)kX3Blk, kX3Bx,
+                 &b_full[s]);
         bulk_g2s(slot + kX3Bx, reinterpret_cast<const uint8_t*>(t.pyz) +
-                                   ((size_t)r * t.ngyz + 4 * (ty - tg.ty0)) * (size_t)kX3Blk,
+                                   ((size_t)r * t.ngyz + (kX3TY / 4) * (ty - tg.ty0)) *
+                                       (size_t)kX3Blk,
                  kX3Byz, &b_full[s]);
       }
 #pragma unroll
@@ -541,10 +551,14 @@ query_x3_kernel(const TcArgs t) {
         mbar_wait(&b_full[s], (uint32_t)(kk & 1));
         tc_fence_after();
         const uint32_t d0 = d_slot + (uint32_t)((kk * H) & 1) * kHid;
-        mma_ss_warp(d0, smem_desc(smem_u32(selx), 128, 256), smem_desc(bx_a, 2048, 128), idesc, 0u);
-        mma_ss_warp(d0, smem_desc(smem_u32(selyz), 128, 512), smem_desc(byz_a, 2048, 128), idesc, 1u);
-        mma_ss_warp(d0, smem_desc(smem_u32(selyz) + 256, 128, 512),
-                    smem_desc(byz_a + 4096, 2048, 128), idesc, 1u);
+#pragma unroll
+        for (int st = 0; st < kX3KX / 16; ++st)       // PX rows of the tile's x-nodes
+          mma_ss_warp(d0, smem_desc(smem_u32(selx) + st * 256, 128, (kX3KX / 8) * 128),
+                      smem_desc(bx_a + st * 4096, 2048, 128), idesc, st ? 1u : 0u);
+#pragma unroll
+        for (int st = 0; st < kX3KYZ / 16; ++st)      // PYZ rows of the tile's (y, z)-rows
+          mma_ss_warp(d0, smem_desc(smem_u32(selyz) + st * 256, 128, (kX3KYZ / 8) * 128),
+                      smem_desc(byz_a + st * 4096, 2048, 128), idesc, 1u);
 #pragma unroll
         for (int st = 0; st < 2; ++st) {
           const uint64_t bh = smem_desc(wlat_hi + st * 256, 128, 512);
@@ -628,8 +642,8 @@ query_x3_kernel(const TcArgs t) {
           if (ch == 0) {
             int r, tx, ty;
             decode(first + kk * tile_stride, r, tx, ty);
-            const int ix = kX3TX * tx + (wtid & 7);
-            const int row = kX3TY * ty + (wtid >> 3);
+            const int ix = kX3TX * tx + (wtid % kX3TX);
+            const int row = kX3TY * ty + (wtid / kX3TX);
             const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
             const float z = part + dotx[s * kTileM + wtid] + bias_out;
             if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {

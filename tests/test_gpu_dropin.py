@@ -89,6 +89,11 @@ def test_embed_bitwise_vs_oracle():
     got = m1.embed_nodes("mu", w1.dims, v0, v1).cpu().numpy()
     want = O.embed(O.grid_positions_of(w1.dims, np.arange(v0, v1)), m1.grid_mu, 6)
     assert np.array_equal(got, want)
+    # the reference family (HashGrid levels) over grid nodes: the generic per-point route
+    dims = (9, 7, 3)
+    hs = O.HashGridSpec(refd.grid_nu, tuple(refd.spec.level_resolutions()), refd.spec.log2_table_size)
+    got = refd.embed_nodes("nu", dims).cpu().numpy()
+    assert np.array_equal(got, O.embed(O.grid_positions(dims), hs, refd.spec.fourier_octaves))
     with pytest.raises(ndf.ParameterError):
         m1.embed(np.zeros_like(m1.grid_mu), pts)
     assert m1.embed("mu", np.zeros((0, 3))).shape == (0, 55)

@@ -5,7 +5,7 @@ import numpy as np, torch
 import paper_2307_02203_b200 as ndf
 from paper_2307_02203_b200 import workloads as W
 w = W.CONFIGS[1]
-model = W.build_model(w, seed=0, grid_init=1e-4).with_precision("fp16")
+model = W.build_model(w, seed=0, grid_init=1e-4).with_precision(os.environ.get("PREC", "bf16"))
 ref = w.ref_position()
 for _ in range(20): ndf.reconstruct_field(model, ref, ndf.ROLE_MU, w.dims)
 torch.cuda.synchronize()
