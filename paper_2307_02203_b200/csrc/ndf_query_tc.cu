@@ -1007,7 +1007,7 @@ query_pp_kernel(const TcArgs t) {
   uint64_t* d_free = &bars[1 + 2 * kPPSlots];     // [kPPSlots] next tile's D half drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   float* eref_s = reinterpret_cast<float*>(bars + 16);      // reference latent channels
-  float* dotx = reinterpret_cast<float*>(bars + 32);        // [kPPSlots][128] partial dots
+  float* dotx = reinterpret_cast<float*>(bars + 32);  // [2 tile parities][kPPSlots][128] partials
 
   const int tid = threadIdx.x;
   const int warp = warp_uniform(tid >> 5);
@@ -1297,14 +1297,14 @@ query_pp_kernel(const TcArgs t) {
           }
           tc_fence_before();
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
-          if (ch == 1) dotx[s * kTileM + wtid] = part;
+          if (ch == 1) dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] = part;
           named_bar(9 + s, 256);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
           if (ch == 0) {
             const int64_t tile_g = first + kk * tile_stride;
             const int64_t r = t.n_ref == 1 ? 0 : (int64_t)((uint32_t)tile_g / (uint32_t)n_vt);
             const int64_t vloc = (tile_g - r * n_vt) * kTileM + wtid;
-            const float z = part + dotx[s * kTileM + wtid] + bias_out;
+            const float z = part + dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] + bias_out;
             if (vloc < n) {
               const float o = head_exact(a.m.head, z);
               if (t.out16) {
@@ -1315,7 +1315,7 @@ query_pp_kernel(const TcArgs t) {
               }
             }
           }
-          named_bar(9 + s, 256);                      // dotx consumed before the next tile
+          // no second barrier: dotx is double-buffered by tile parity (see x3)
           NDF_TRACE_AT((int)kk, 6);
         }
       }
@@ -1652,7 +1652,7 @@ static int launch_pp_t(const tc::TcArgs& t, cudaStream_t s) {
   const tc::Layout lay = tc::make_layout(t.q.m);
   const size_t smem_pp = (size_t)((lay.blob_bytes + 1023) & ~1023) +
                          (size_t)tc::kPPSlots * tc::kABytes +
-                         (size_t)(1 + lay.H) * tc::kBiasBlk + 2048;
+                         (size_t)(1 + lay.H) * tc::kBiasBlk + 2304;
   static SmemAttrCache attr;
   NDF_CUDA_CHECK(attr.ensure(tc::query_pp_kernel<F16, SILU>, smem_pp));
   NDF_CUDA_CHECK(launch_pdl(tc::query_pp_kernel<F16, SILU>, g2, tc::kPPThreads, smem_pp, s, t));
@@ -1738,7 +1738,10 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
     cudaError_t e = cudaGetLastError();
     const float* featc = feat;
     if (e == cudaSuccess)
-      e = launch_pdl(tc::prep_x3_tab_kernel, (unsigned)((int64_t)n_ref * (ngx + ngyz)), 128, 0, s, a, n_ref,
+      e = launch_pdl(tc::prep_x3_tab_kernel,
+                     (unsigned)((int64_t)n_ref * ((ngx + tc::kX3TabG - 1) / tc::kX3TabG +
+                                                   (ngyz + tc::kX3TabG - 1) / tc::kX3TabG)),
+                     128, 0, s, a, n_ref,
                      featc, ngx, ngyz, (int64_t)tg.ty0 * tc::kX3TY, px, pyz);
     count_launch();
     const int64_t tiles = tg.n_vt * n_ref;

@@ -74,7 +74,7 @@ __host__ __device__ inline X3Layout make_x3_layout(const ndf_model_desc& m) {
   x.wout32 = x.wh_lo + (lay.H - 1) * lay.wh_bytes;
   x.ext_bytes = x.wout32 + kHid * 4;
   x.smem_w = ((lay.H - 1) * lay.wh_bytes + x.ext_bytes + 1023) & ~1023;
-  x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2048;
+  x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2304;
   return x;
 }
 
@@ -93,8 +93,9 @@ __device__ __forceinline__ uint32_t split_f32(float v) {
   return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
 }
 
-// Per-query layer-0 tables, one 128-thread block per (reference r, 4-node group g), thread
-// = output feature n: the 4 nodes' values as (hi, lo) words, 16 B at
+// Per-query layer-0 tables, one 128-thread block per (reference r, kX3TabG consecutive 4-node
+// groups g of one kind) -- 16 nodes share every weight load -- thread = output feature n:
+// a group's 4 nodes' values as (hi, lo) words, 16 B at
 // ((r * ng + g) * 128 + n) * 16.  Groups [0, ngx) are x-nodes 4g + j (PX: raw x and
 // Fourier-x features); groups g = ngx + g' are (y, z)-rows row0 + 4 g' + j with
 // row = iy + ny * iz (PYZ: raw y, z, Fourier-y, z, plus the bias) -- only the rows of the
@@ -102,73 +103,102 @@ __device__ __forceinline__ uint32_t split_f32(float v) {
 // in fp32 exactly as the reference merge (r + q, |r - q|; model.py:279-286 + BASELINE)
 // and weighted with fp32 FMAs (pre-scaled by 1/2 for SiLU): their ~2^-21 relative error
 // sits far below the 2^-17 of the hi + lo pair the sum is stored as.
+constexpr int kX3TabG = 4;          // 4-node groups per prep block (16 nodes share each W load)
+
 __global__ void __launch_bounds__(128)
 prep_x3_tab_kernel(const QueryArgs a, int n_ref, const float* __restrict__ feat, int ngx,
                    int ngyz, int64_t row0, uint4* px, uint4* pyz) {
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");      // feat from prep_ws_feat_kernel
-  __shared__ float qf[4][2][16];   // node j's axis features (x nodes: [0]; rows: y [0], z [1])
-  __shared__ float rf[3][16];      // the reference's x, y, z features
-  const int per_ref = ngx + ngyz;
-  const int r = blockIdx.x / per_ref, g = blockIdx.x - r * per_ref;
+  constexpr int kN = 4 * kX3TabG;   // nodes per block
+  constexpr int kF = 26;            // features per block: 13 (x blocks) or 26 (y / z blocks)
+  // merged inputs of the block's nodes, feature-major so a node pair is one 8-byte load:
+  // sm = r + q, dm = |r - q| (fp32, exactly the reference merge, model.py:279-286)
+  __shared__ __align__(16) float sm[kF][kN];
+  __shared__ __align__(16) float dm[kF][kN];
+  const int bx = (ngx + kX3TabG - 1) / kX3TabG, byz = (ngyz + kX3TabG - 1) / kX3TabG;
+  const int per_ref = bx + byz;
+  const int r = blockIdx.x / per_ref, b = blockIdx.x - r * per_ref;
   const int n = threadIdx.x;
-  const bool isx = g < ngx;
+  const bool isx = b < bx;
+  const int g0 = kX3TabG * (isx ? b : b - bx);          // first group of this block
+  const int ng = isx ? ngx : ngyz;
   const int nyz = a.ny * a.nz;
-  {
-    const int j = n >> 5, ax = (n >> 4) & 1, c = n & 15;
-    float v = 0.0f;
-    if (isx) {
-      const int ix = 4 * g + j;
-      if (ax == 0 && ix < a.nx) v = feat[(size_t)ix * 16 + c];
-    } else {
-      const int64_t row = row0 + 4 * (g - ngx) + j;
-      if (row < nyz) {
-        const int node = ax == 0 ? a.nx + (int)(row % a.ny) : a.nx + a.ny + (int)(row / a.ny);
-        v = feat[(size_t)node * 16 + c];
+  const int nf = isx ? 1 + 2 * kL : 2 + 4 * kL;
+  const int nref = a.nx + a.ny + a.nz + 3 * r;          // reference r's x node in feat
+  // feature i of this block -> (feature-table column c, reference axis, query axis)
+  auto fmap = [&](int i, int& c, int& rax, int& qaxis) {
+    if (isx) { c = i; rax = 0; qaxis = 0; return; }          // raw x, then sin / cos per octave
+    if (i < 2) { c = 0; rax = 1 + i; qaxis = i; return; }   // raw y, raw z
+    const int j = i - 2, o = j >> 2, ax = 1 + ((j >> 1) & 1), sc = j & 1;
+    c = 1 + 2 * o + sc; rax = ax; qaxis = ax - 1;
+  };
+  for (int k = n; k < kN * kF; k += 128) {
+    const int i = k / kN, j = k - i * kN;
+    float sv = 0.0f, dv = 0.0f;
+    if (i < nf) {
+      int c, rax, qaxis;
+      fmap(i, c, rax, qaxis);
+      int node = -1;
+      if (isx) {
+        const int ix = 4 * g0 + j;
+        if (ix < a.nx) node = ix;
+      } else {
+        const int64_t row = row0 + 4 * g0 + j;
+        if (row < nyz) node = qaxis == 0 ? a.nx + (int)(row % a.ny) : a.nx + a.ny + (int)(row / a.ny);
+      }
+      if (node >= 0) {
+        const float rv = feat[(size_t)(nref + rax) * 16 + c];
+        const float qv = feat[(size_t)node * 16 + c];
+        sv = rv + qv;
+        dv = fabsf(rv - qv);
       }
     }
-    qf[j][ax][c] = v;
-    const int nref = a.nx + a.ny + a.nz + 3 * r;   // reference r's x node in feat
-    if (n < 48) rf[n >> 4][n & 15] = feat[(size_t)(nref + (n >> 4)) * 16 + (n & 15)];
+    sm[i][j] = sv;
+    dm[i][j] = dv;
   }
   __syncthreads();
+  // thread n = output feature: its weights for the block's features, then packed FMAs over
+  // node pairs (fp32; the hi + lo pair the sum is stored as keeps 2^-17)
   const float* W = a.m.params_f32;                 // W0: (2E x 128) row-major, then b0
-  float v[4];
-  // feature f of axis ax, stored at column c of the axis rows
-  auto add = [&](int f, int ax, int qax, int c) {
-    const float ws = __ldg(W + (size_t)f * kHid + n), wd = __ldg(W + (size_t)(kE + f) * kHid + n);
-    const float rv = rf[ax][c];
+  float v[kN];
+  const float v0 = isx ? 0.0f : __ldg(W + (size_t)2 * kE * kHid + n);   // bias in PYZ
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float qv = qf[j][qax][c];
-      v[j] = fmaf(wd, fabsf(rv - qv), fmaf(ws, rv + qv, v[j]));
-    }
-  };
-  bool valid[4];
-  if (isx) {
+  for (int j = 0; j < kN; ++j) v[j] = v0;
+  // all weight loads in flight at once (one L2 round trip), then FMAs from registers
+  float ws[kF], wd[kF];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { v[j] = 0.0f; valid[j] = 4 * g + j < a.nx; }
-    add(0, 0, 0, 0);
+  for (int i = 0; i < kF; ++i) {
+    const int f = isx ? (i == 0 ? 0 : 3 + 6 * ((i - 1) >> 1) + ((i - 1) & 1))
+                      : (i < 2 ? 1 + i : 3 + 6 * ((i - 2) >> 2) + 2 * (1 + (((i - 2) >> 1) & 1)) + ((i - 2) & 1));
+    ws[i] = i < nf ? __ldg(W + (size_t)f * kHid + n) : 0.0f;
+    wd[i] = i < nf ? __ldg(W + (size_t)(kE + f) * kHid + n) : 0.0f;
+  }
 #pragma unroll
-    for (int o = 0; o < kL; ++o) { add(3 + 6 * o, 0, 0, 1 + 2 * o); add(4 + 6 * o, 0, 0, 2 + 2 * o); }
-  } else {
-    const float bias = __ldg(W + (size_t)2 * kE * kHid + n);
+  for (int i = 0; i < kF; ++i) {
+    if (i >= nf) break;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { v[j] = bias; valid[j] = row0 + 4 * (g - ngx) + j < nyz; }
-    add(1, 1, 0, 0);
-    add(2, 2, 1, 0);
-#pragma unroll
-    for (int o = 0; o < kL; ++o) {
-      add(5 + 6 * o, 1, 0, 1 + 2 * o); add(6 + 6 * o, 1, 0, 2 + 2 * o);
-      add(7 + 6 * o, 2, 1, 1 + 2 * o); add(8 + 6 * o, 2, 1, 2 + 2 * o);
+    for (int j = 0; j < kN; j += 2) {
+      const float2 s2 = *reinterpret_cast<const float2*>(&sm[i][j]);
+      const float2 d2 = *reinterpret_cast<const float2*>(&dm[i][j]);
+      ffma2(v[j], v[j + 1], ws[i], ws[i], s2.x, s2.y, v[j], v[j + 1]);
+      ffma2(v[j], v[j + 1], wd[i], wd[i], d2.x, d2.y, v[j], v[j + 1]);
     }
   }
   const float hs = a.m.activation == NDF_ACT_SILU ? 0.5f : 1.0f;
-  uint32_t w[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) w[j] = valid[j] ? split_f32(v[j] * hs) : 0u;
-  uint4* dst = isx ? px + ((size_t)r * ngx + g) * kHid : pyz + ((size_t)r * ngyz + (g - ngx)) * kHid;
-  dst[n] = make_uint4(w[0], w[1], w[2], w[3]);
+  for (int gi = 0; gi < kX3TabG; ++gi) {
+    const int g = g0 + gi;
+    if (g >= ng) break;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool valid = isx ? 4 * g + j < a.nx : row0 + 4 * g + j < nyz;
+      w[j] = valid ? split_f32(v[4 * gi + j] * hs) : 0u;
+    }
+    uint4* dst = isx ? px + ((size_t)r * ngx + g) * kHid : pyz + ((size_t)r * ngyz + g) * kHid;
+    dst[n] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 // Fill the blob extension (after pack_fill_kernel has written the standard layout).
@@ -348,7 +378,7 @@ query_x3_kernel(const TcArgs t) {
   uint64_t* b_full = &bars[7];                    // [kPPSlots] the tile's PX / PYZ rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   float* eref_s = reinterpret_cast<float*>(bars + 16);
-  float* dotx = reinterpret_cast<float*>(bars + 32);
+  float* dotx = reinterpret_cast<float*>(bars + 32);     // [2 tile parities][kPPSlots][128]
 
   const int tid = threadIdx.x;
   const int warp = warp_uniform(tid >> 5);
@@ -461,11 +491,17 @@ query_x3_kernel(const TcArgs t) {
           const uint32_t whi = smem_u32(wh_s) + (uint32_t)(l * lay.wh_bytes);
           const uint32_t wlo = smem_u32(ext_s) + (uint32_t)(xl.wh_lo + l * lay.wh_bytes);
           const bool use_lo = (wlo_mask >> (l + 1)) & 1u;
-          if (t.x3_burst)      // whole layer after the epilogue (K-chunk barriers passed first)
+          // x3_burst: 0 = issue K-chunk by K-chunk as the epilogue completes them,
+          // 1 = the whole layer after the epilogue, 2 = pairs of K-chunks
+          if (t.x3_burst == 1)
             for (int k2 = 0; k2 < 4; ++k2) named_bar(1 + 4 * si + k2, 288);
 #pragma unroll 1
           for (int k2 = 0; k2 < 4; ++k2) {
-            if (!t.x3_burst) named_bar(1 + 4 * si + k2, 288);
+            if (t.x3_burst == 0) named_bar(1 + 4 * si + k2, 288);
+            if (t.x3_burst == 2 && (k2 & 1) == 0) {
+              named_bar(1 + 4 * si + k2, 288);
+              named_bar(1 + 4 * si + k2 + 1, 288);
+            }
             // the whole issuer warp runs this (elect.sync inside the MMA asm): operands
             // stay in uniform registers, MMAs go out back to back
             tc_fence_after();
@@ -637,7 +673,7 @@ query_x3_kernel(const TcArgs t) {
           }
           tc_fence_before();
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
-          if (ch == 1) dotx[s * kTileM + wtid] = part;
+          if (ch == 1) dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] = part;
           named_bar(9 + s, 256);
           if (ch == 0) {
             int r, tx, ty;
@@ -645,7 +681,7 @@ query_x3_kernel(const TcArgs t) {
             const int ix = kX3TX * tx + (wtid % kX3TX);
             const int row = kX3TY * ty + (wtid / kX3TX);
             const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
-            const float z = part + dotx[s * kTileM + wtid] + bias_out;
+            const float z = part + dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] + bias_out;
             if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {
               const float o = head_exact(a.m.head, z);
               if (t.out16) {
@@ -656,7 +692,9 @@ query_x3_kernel(const TcArgs t) {
               }
             }
           }
-          named_bar(9 + s, 256);
+          // no second barrier: dotx is double-buffered by tile parity, so the column-1
+          // warps may run ahead into the next tile (they pass the next barrier only after
+          // the column-0 warps finished reading this buffer)
           if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
         }
       }
