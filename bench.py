@@ -454,7 +454,7 @@ def run_ours(args):
         sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
         sm_hz = ((clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
         sfu_floor_ms = SFU_OPS_PER_PAIR * (v1 - v0) / (SFU_PER_CLK_SM * sm_count * sm_hz) * 1e3
-        kname = {"bf16": "ndf::tc::query_x3_kernel (+ prep_ws_feat_kernel, prep_x3_tab_kernel)",
+        kname = {"bf16": "ndf::tc::query_x3_kernel (+ prep_x3_kernel)",
                  "fp16": "ndf::tc::query_pp_kernel (+ prep_ws_feat_kernel, prep_ws_merge_kernel)",
                  "fp32": "ndf::query_f32_kernel (+ prep)"}[args.precision]
         roof = {"bound": "tensor", "kernel": kname,

@@ -1683,10 +1683,9 @@ static int launch_tc_variant(const tc::TcArgs& t, int nwg, size_t smem, unsigned
 // only used by the multi-reference entry point.
 static long long* g_trace = nullptr;   // debug hook (ndf_debug_tc_trace)
 
-// bf16 grid query on the split-operand kernel: prep_ws_feat_kernel (axis features,
-// reference latent channels, z-interpolated latent rows) -> prep_x3_tab_kernel (PX / PYZ
-// layer-0 tables per reference) -> query_x3_kernel, chained by programmatic dependent
-// launch.  NDF_X3_WLO (bitmask of hidden layers, default all) selects which hidden
+// bf16 grid query on the split-operand kernel: prep_x3_kernel (PX / PYZ layer-0 tables per
+// reference, z-interpolated latent rows, reference latent channels; one launch) ->
+// query_x3_kernel (programmatic dependent launch: its prologue overlaps the prep).  NDF_X3_WLO (bitmask of hidden layers, default all) selects which hidden
 // layers run the A_hi x W_lo term -- a timing / accuracy experiment knob.
 static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t s) {
   const QueryArgs& a = t.q;
@@ -1702,15 +1701,15 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
     burst = e ? atoi(e) : 0;
   }
   t.x3_burst = burst;
-  const int nnode = a.nx + a.ny + a.nz + 3 * n_ref;
   const int ngx = (a.nx + tc::kX3TX - 1) / tc::kX3TX * (tc::kX3TX / 4);
   const tc::X3Tiles tg = tc::x3_tiles(a.nx, a.v0, a.v1);
   const int64_t ngyz64 = tg.n_vt / (tg.n_xt) * (tc::kX3TY / 4);   // this launch's row-tiles
   NDF_REQUIRE(ngyz64 < (1LL << 30), NDF_ERR_UNSUPPORTED, "too many (y, z) rows for the bf16 path");
   const int ngyz = (int)ngyz64;
-  NDF_REQUIRE((int64_t)n_ref * (ngx + ngyz) < (1LL << 31), NDF_ERR_UNSUPPORTED,
+  NDF_REQUIRE((int64_t)n_ref * (ngx + ngyz) + (int64_t)a.nz * a.g.ry * a.g.rx / 128 + n_ref <
+                  (1LL << 31), NDF_ERR_UNSUPPORTED,
               "too many reference x table groups for one bf16 launch");
-  const size_t fb = ((size_t)nnode * 16 * 4 + 255) & ~(size_t)255;
+  const size_t fb = 0;
   const size_t lb = ((size_t)a.nz * a.g.ry * a.g.rx * tc::kC * 4 + 255) & ~(size_t)255;
   const size_t eb = ((size_t)n_ref * tc::kERefStride * 4 + 255) & ~(size_t)255;
   const size_t xb = (size_t)n_ref * ngx * tc::kX3Blk;
@@ -1718,7 +1717,6 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
   void* scratch = nullptr;
   NDF_CUDA_CHECK(scratch_alloc(&scratch, fb + lb + eb + xb + yb, s));
   uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
-  float* feat = reinterpret_cast<float*>(p);
   float* lt = reinterpret_cast<float*>(p + fb);
   float* et = reinterpret_cast<float*>(p + fb + lb);
   uint4* px = reinterpret_cast<uint4*>(p + fb + lb + eb);
@@ -1731,19 +1729,15 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
   t.ngyz = ngyz;
   int st = NDF_OK;
   do {
-    const int64_t n1 = (int64_t)nnode * tc::kL + n_ref + (int64_t)a.nz * a.g.ry * a.g.rx;
-    tc::prep_ws_feat_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(a, refs_dev, n_ref, feat,
-                                                                          et, lt);
+    // one prep launch (tables, z-interpolated latent rows, reference latent channels)
+    const int64_t nT = (int64_t)n_ref * ((ngx + tc::kX3TabG - 1) / tc::kX3TabG +
+                                         (ngyz + tc::kX3TabG - 1) / tc::kX3TabG);
+    const int64_t nL = ((int64_t)a.nz * a.g.ry * a.g.rx + 127) / 128;
+    const int64_t nR = (n_ref + 127) / 128;
+    tc::prep_x3_kernel<<<(unsigned)(nT + nL + nR), 128, 0, s>>>(
+        a, refs_dev, n_ref, ngx, ngyz, (int64_t)tg.ty0 * tc::kX3TY, px, pyz, et, lt);
     count_launch();
     cudaError_t e = cudaGetLastError();
-    const float* featc = feat;
-    if (e == cudaSuccess)
-      e = launch_pdl(tc::prep_x3_tab_kernel,
-                     (unsigned)((int64_t)n_ref * ((ngx + tc::kX3TabG - 1) / tc::kX3TabG +
-                                                   (ngyz + tc::kX3TabG - 1) / tc::kX3TabG)),
-                     128, 0, s, a, n_ref,
-                     featc, ngx, ngyz, (int64_t)tg.ty0 * tc::kX3TY, px, pyz);
-    count_launch();
     const int64_t tiles = tg.n_vt * n_ref;
     const unsigned g2 = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));

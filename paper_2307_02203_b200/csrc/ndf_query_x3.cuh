@@ -12,7 +12,7 @@
 //   (raw y/z, Fourier-y/z), so its pre-activation is
 //       z0 = PX[ix] + PYZ[iy, iz] + W_lat^T [r + lat, |r - lat|]
 //   with PX / PYZ (bias folded into PYZ) computed per query in fp64 by
-//   prep_x3_tab_kernel from the fp32 merged features and fp32 weights, stored as
+//   prep_x3_kernel from the fp32 merged features and fp32 weights, stored as
 //   bf16 hi + lo pairs (16 significant bits).  A tile is 16 x-nodes x 8 (y, z)-rows,
 //   so PX and PYZ enter the accumulator through two constant one-hot selector blocks
 //   (A = [1 1] in the columns of the row's node, B = the tile's 16 PX / 8 PYZ rows,
@@ -93,90 +93,169 @@ __device__ __forceinline__ uint32_t split_f32(float v) {
   return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
 }
 
-// Per-query layer-0 tables, one 128-thread block per (reference r, kX3TabG consecutive 4-node
-// groups g of one kind) -- 16 nodes share every weight load -- thread = output feature n:
-// a group's 4 nodes' values as (hi, lo) words, 16 B at
-// ((r * ng + g) * 128 + n) * 16.  Groups [0, ngx) are x-nodes 4g + j (PX: raw x and
-// Fourier-x features); groups g = ngx + g' are (y, z)-rows row0 + 4 g' + j with
-// row = iy + ny * iz (PYZ: raw y, z, Fourier-y, z, plus the bias) -- only the rows of the
-// launch's row-tiles.  Nodes / rows past the grid are zero.  The merged values are formed
-// in fp32 exactly as the reference merge (r + q, |r - q|; model.py:279-286 + BASELINE)
-// and weighted with fp32 FMAs (pre-scaled by 1/2 for SiLU): their ~2^-21 relative error
-// sits far below the 2^-17 of the hi + lo pair the sum is stored as.
 constexpr int kX3TabG = 4;          // 4-node groups per prep block (16 nodes share each W load)
 
+// PX / PYZ tables, per reference r: groups of 4 nodes, [n = 0..127][node][hi, lo] bf16 (16 B per
+// (group, n)) at ((r * ng + g) * 128 + n) * 16; x-groups (PX: raw x and Fourier-x features) and
+// (y, z)-row groups row0 + 4 g + j, row = iy + ny * iz (PYZ: raw y, z, Fourier-y, z, plus the
+// bias), only the rows of the launch's row-tiles; nodes / rows past the grid are zero.  The
+// merged values are formed in fp32 exactly as the reference merge (r + q, |r - q|,
+// model.py:279-286 + BASELINE) and weighted with fp32 FMAs (pre-scaled by 1/2 for SiLU):
+// their ~2^-21 relative error sits far below the 2^-17 of the hi + lo pair they are stored as.
+//
+// The whole per-query prep of the bf16 query in ONE launch (blocks of 128 threads):
+//   [0, nT)            PX / PYZ table blocks: each computes the axis features it needs (one
+//                      fp64 sincos per node x octave, the operations of prep_ws_feat_kernel /
+//                      embed_point_t, so the same bits), stages the merged inputs of its 16
+//                      nodes, and runs the weighted sums (see below)
+//   [nT, nT + nL)      lz: the query grid's latent rows interpolated along z (fp32)
+//   [nT + nL, ...)     the references' latent channels in fp64 (embed_point_t's corner order)
+// One launch instead of two serialized ones (round 2: prep_ws_feat_kernel -> prep_x3_tab_kernel).
+__device__ __forceinline__ double clamp1(double p) { return fmin(fmax(p, -1.0), 1.0); }
+
 __global__ void __launch_bounds__(128)
-prep_x3_tab_kernel(const QueryArgs a, int n_ref, const float* __restrict__ feat, int ngx,
-                   int ngyz, int64_t row0, uint4* px, uint4* pyz) {
+prep_x3_kernel(const QueryArgs a, const double* refs, int n_ref, int ngx, int ngyz, int64_t row0,
+               uint4* px, uint4* pyz, float* eref_lat, float* lz) {
   asm volatile("griddepcontrol.launch_dependents;");
-  asm volatile("griddepcontrol.wait;" ::: "memory");      // feat from prep_ws_feat_kernel
-  constexpr int kN = 4 * kX3TabG;   // nodes per block
+  constexpr int kN = 4 * kX3TabG;   // nodes per table block
   constexpr int kF = 26;            // features per block: 13 (x blocks) or 26 (y / z blocks)
-  // merged inputs of the block's nodes, feature-major so a node pair is one 8-byte load:
-  // sm = r + q, dm = |r - q| (fp32, exactly the reference merge, model.py:279-286)
+  constexpr int kSlots = 2 * kN + 2;   // node-feature slots: x: 16 nodes + ref x; yz: 16 y,
+                                       // 16 z, ref y, ref z
+  __shared__ float nf[kSlots][1 + 2 * kL];
   __shared__ __align__(16) float sm[kF][kN];
   __shared__ __align__(16) float dm[kF][kN];
   const int bx = (ngx + kX3TabG - 1) / kX3TabG, byz = (ngyz + kX3TabG - 1) / kX3TabG;
   const int per_ref = bx + byz;
-  const int r = blockIdx.x / per_ref, b = blockIdx.x - r * per_ref;
+  const int64_t nT = (int64_t)n_ref * per_ref;
+  const int64_t nlz = (int64_t)a.nz * a.g.ry * a.g.rx;
+  const int64_t nL = (nlz + 127) / 128;
   const int n = threadIdx.x;
+  if ((int64_t)blockIdx.x >= nT) {
+    const int64_t bb = (int64_t)blockIdx.x - nT;
+    if (bb < nL) {                              // ---- lz rows (query branch grid) ----
+      const int64_t k = bb * 128 + n;
+      if (k >= nlz) return;
+      const int cx = (int)(k % a.g.rx), cy = (int)((k / a.g.rx) % a.g.ry);
+      const int iz = (int)(k / ((int64_t)a.g.rx * a.g.ry));
+      int z0;
+      float tz;
+      latent_cell(iz, a.nz, a.g.rz, z0, tz);
+      const float* grid = a.ref_is_mu ? a.m.grid_nu : a.m.grid_mu;
+      const float4* p0 = reinterpret_cast<const float4*>(
+          grid + ((size_t)(z0 * a.g.ry + cy) * a.g.rx + cx) * kC);
+      const float4* p1 = p0 + (size_t)a.g.ry * a.g.rx * kC / 4;
+      float4* dst = reinterpret_cast<float4*>(lz + (size_t)k * kC);
+#pragma unroll
+      for (int q = 0; q < kC / 4; ++q) {
+        const float4 f = __ldg(p0 + q), h = __ldg(p1 + q);
+        dst[q] = make_float4(fmaf(tz, h.x - f.x, f.x), fmaf(tz, h.y - f.y, f.y),
+                             fmaf(tz, h.z - f.z, f.z), fmaf(tz, h.w - f.w, f.w));
+      }
+      return;
+    }
+    const int r = (int)((bb - nL) * 128 + n);   // ---- reference latent channels ----
+    if (r >= n_ref) return;
+    const double* rp = refs ? refs + 3 * r : a.ref;
+    const float* grid = a.ref_is_mu ? a.m.grid_mu : a.m.grid_nu;
+    const double p[3] = {clamp1(rp[0]), clamp1(rp[1]), clamp1(rp[2])};
+    const AxisCoord cx = level_coord(p[0], a.g.rx);
+    const AxisCoord cy = level_coord(p[1], a.g.ry);
+    const AxisCoord cz = level_coord(p[2], a.g.rz);
+    double acc[kC];
+#pragma unroll
+    for (int ch = 0; ch < kC; ++ch) acc[ch] = 0.0;
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+      const double wx = dx ? cx.t : dsub(1.0, cx.t);
+      const double wy = dy ? cy.t : dsub(1.0, cy.t);
+      const double wz = dz ? cz.t : dsub(1.0, cz.t);
+      const double w = dmul(dmul(wx, wy), wz);
+      const int idx = (cx.i0 + dx) + a.g.rx * ((cy.i0 + dy) + a.g.ry * (cz.i0 + dz));
+#pragma unroll
+      for (int ch = 0; ch < kC; ++ch)
+        acc[ch] = dadd(acc[ch], dmul(w, (double)__ldg(grid + (size_t)idx * kC + ch)));
+    }
+    for (int ch = 0; ch < kC; ++ch) eref_lat[(size_t)r * kERefStride + ch] = (float)acc[ch];
+    return;
+  }
+  // ---- PX / PYZ table block ----
+  const int r = blockIdx.x / per_ref, b = blockIdx.x - r * per_ref;
   const bool isx = b < bx;
-  const int g0 = kX3TabG * (isx ? b : b - bx);          // first group of this block
+  const int g0 = kX3TabG * (isx ? b : b - bx);
   const int ng = isx ? ngx : ngyz;
   const int nyz = a.ny * a.nz;
-  const int nf = isx ? 1 + 2 * kL : 2 + 4 * kL;
-  const int nref = a.nx + a.ny + a.nz + 3 * r;          // reference r's x node in feat
-  // feature i of this block -> (feature-table column c, reference axis, query axis)
-  auto fmap = [&](int i, int& c, int& rax, int& qaxis) {
-    if (isx) { c = i; rax = 0; qaxis = 0; return; }          // raw x, then sin / cos per octave
-    if (i < 2) { c = 0; rax = 1 + i; qaxis = i; return; }   // raw y, raw z
-    const int j = i - 2, o = j >> 2, ax = 1 + ((j >> 1) & 1), sc = j & 1;
-    c = 1 + 2 * o + sc; rax = ax; qaxis = ax - 1;
-  };
+  const int nslot = isx ? kN + 1 : 2 * kN + 2;
+  const double* rp = refs ? refs + 3 * r : a.ref;
+  for (int item = n; item < nslot * (kL + 1); item += 128) {
+    const int q = item / (kL + 1), o = item - q * (kL + 1);
+    double p = 0.0;
+    bool ok = true;
+    if (isx) {
+      if (q < kN) {
+        const int ix = 4 * g0 + q;
+        ok = ix < a.nx;
+        p = ok ? node_coord(ix, a.nx) : 0.0;
+      } else {
+        p = rp[0];
+      }
+    } else if (q < 2 * kN) {
+      const int64_t row = row0 + 4 * g0 + (q % kN);
+      ok = row < nyz;
+      if (ok) p = q < kN ? node_coord((int)(row % a.ny), a.ny) : node_coord((int)(row / a.ny), a.nz);
+    } else {
+      p = rp[1 + (q - 2 * kN)];
+    }
+    p = clamp1(p);
+    if (o == kL) {
+      nf[q][0] = ok ? (float)p : 0.0f;
+    } else {
+      double scale = 3.141592653589793;
+      for (int i = 0; i < o; ++i) scale = scale * 2.0;
+      double sn, cs;
+      sincos(dmul(scale, p), &sn, &cs);
+      nf[q][1 + 2 * o] = ok ? (float)sn : 0.0f;
+      nf[q][2 + 2 * o] = ok ? (float)cs : 0.0f;
+    }
+  }
+  __syncthreads();
+  const int nfeat = isx ? 1 + 2 * kL : 2 + 4 * kL;
   for (int k = n; k < kN * kF; k += 128) {
     const int i = k / kN, j = k - i * kN;
     float sv = 0.0f, dv = 0.0f;
-    if (i < nf) {
-      int c, rax, qaxis;
-      fmap(i, c, rax, qaxis);
-      int node = -1;
-      if (isx) {
-        const int ix = 4 * g0 + j;
-        if (ix < a.nx) node = ix;
+    if (i < nfeat) {
+      int c, rslot, qslot;
+      if (isx) {                         // raw x, then sin / cos per octave
+        c = i; rslot = kN; qslot = j;
+      } else if (i < 2) {                // raw y, raw z
+        c = 0; rslot = 2 * kN + i; qslot = i * kN + j;
       } else {
-        const int64_t row = row0 + 4 * g0 + j;
-        if (row < nyz) node = qaxis == 0 ? a.nx + (int)(row % a.ny) : a.nx + a.ny + (int)(row / a.ny);
+        const int jj = i - 2, o = jj >> 2, ax = 1 + ((jj >> 1) & 1), sc = jj & 1;
+        c = 1 + 2 * o + sc; rslot = 2 * kN + ax - 1; qslot = (ax - 1) * kN + j;
       }
-      if (node >= 0) {
-        const float rv = feat[(size_t)(nref + rax) * 16 + c];
-        const float qv = feat[(size_t)node * 16 + c];
-        sv = rv + qv;
-        dv = fabsf(rv - qv);
-      }
+      const float rv = nf[rslot][c], qv = nf[qslot][c];
+      sv = rv + qv;
+      dv = fabsf(rv - qv);
     }
     sm[i][j] = sv;
     dm[i][j] = dv;
   }
   __syncthreads();
-  // thread n = output feature: its weights for the block's features, then packed FMAs over
-  // node pairs (fp32; the hi + lo pair the sum is stored as keeps 2^-17)
   const float* W = a.m.params_f32;                 // W0: (2E x 128) row-major, then b0
   float v[kN];
   const float v0 = isx ? 0.0f : __ldg(W + (size_t)2 * kE * kHid + n);   // bias in PYZ
 #pragma unroll
   for (int j = 0; j < kN; ++j) v[j] = v0;
-  // all weight loads in flight at once (one L2 round trip), then FMAs from registers
   float ws[kF], wd[kF];
 #pragma unroll
   for (int i = 0; i < kF; ++i) {
     const int f = isx ? (i == 0 ? 0 : 3 + 6 * ((i - 1) >> 1) + ((i - 1) & 1))
                       : (i < 2 ? 1 + i : 3 + 6 * ((i - 2) >> 2) + 2 * (1 + (((i - 2) >> 1) & 1)) + ((i - 2) & 1));
-    ws[i] = i < nf ? __ldg(W + (size_t)f * kHid + n) : 0.0f;
-    wd[i] = i < nf ? __ldg(W + (size_t)(kE + f) * kHid + n) : 0.0f;
+    ws[i] = i < nfeat ? __ldg(W + (size_t)f * kHid + n) : 0.0f;
+    wd[i] = i < nfeat ? __ldg(W + (size_t)(kE + f) * kHid + n) : 0.0f;
   }
 #pragma unroll
   for (int i = 0; i < kF; ++i) {
-    if (i >= nf) break;
+    if (i >= nfeat) break;
 #pragma unroll
     for (int j = 0; j < kN; j += 2) {
       const float2 s2 = *reinterpret_cast<const float2*>(&sm[i][j]);

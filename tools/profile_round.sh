@@ -28,8 +28,7 @@ case "${1:-bench}" in
     echo "launches rc=$?";;
   ncu1)
     prof x3 query_x3 "--import-source on" python tools/x3_probe.py 2
-    prof preptab prep_x3_tab "" python tools/x3_probe.py 2
-    prof prepfeat prep_ws_feat "" python tools/x3_probe.py 2
+    prof preptab prep_x3_kernel "" python tools/x3_probe.py 2
     prof embed "embed_(nodes_)?kernel" "" python tools/embed_probe.py;;
   ncu2)
     prof field pearson_field "" python tools/gemv_probe.py
