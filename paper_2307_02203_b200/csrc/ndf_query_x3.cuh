@@ -428,6 +428,13 @@ __host__ __device__ inline X3Tiles x3_tiles(int nx, int64_t v0, int64_t v1) {
 // schedule trace of CTA 0 (trace builds only, tools/trace_x3.py): t.trace[(slot * 32 + tile)
 // * 24 + event]; producer 0-4, epilogue lead warp 5 + 2l (layer l's MMAs done) / 6 + 2l
 // (its epilogue done), issuer 12 + 4l + k2 (K-chunk k2 of layer l + 1 issued)
+// per-warp stamps (trace builds): layers 0 / 1 of tiles < 32, epilogue warp ch * 4 + wq
+#define NDF_X3_TRACE_W(ev)                                                              \
+  do {                                                                                  \
+    if (NDF_TRACE_ON(blockIdx.x == 0 && kk < 32 && l < 2 && lane == 0))                  \
+      t.trace[2 * 32 * 24 + 300 + ((((s * 32 + (int)kk) * 2 + l) * 8 + ch * 4 + wq) * 8) \
+              + (ev)] = clock64();                                                      \
+  } while (0)
 #define NDF_X3_TRACE(slot_, kk_, ev)                                                    \
   do {                                                                                  \
     if (NDF_TRACE_ON(blockIdx.x == 0 && (kk_) < 32))                                     \
@@ -465,6 +472,17 @@ query_x3_kernel(const TcArgs t) {
   const int wg = warp >> 2;
   const int wq = warp & 3;
   const int wtid = tid & 127;
+  // trace builds: per-CTA globaltimer at entry / exit, CTA 0's clock64 (after the tiles)
+#define NDF_X3_TRACE_CTA(k)                                                              \
+  do {                                                                                  \
+    if (NDF_TRACE_ON(tid == 0 && blockIdx.x < 148)) {                                   \
+      uint64_t gt;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                            \
+      t.trace[2 * 32 * 24 + 2 * blockIdx.x + (k)] = (long long)gt;                      \
+      if (blockIdx.x == 0) t.trace[2 * 32 * 24 + 296 + (k)] = clock64();                \
+    }                                                                                   \
+  } while (0)
+  NDF_X3_TRACE_CTA(0);
 
   if (tid == 0) {
     mbar_init(wbar, 1);
@@ -698,6 +716,29 @@ query_x3_kernel(const TcArgs t) {
         reinterpret_cast<const uint8_t*>(a.m.params_tc) + lay.vec_off) + H * kHid);
     const uint32_t w32_addr = smem_u32(ext_s) + xl.wout32;
     uint32_t acc_ph = 0u;
+    // Output of a finished tile, written late: the column-0 warps keep the row's pre-head
+    // value and store it after the next tile's first epilogue (where they would otherwise
+    // wait on the layer-1 MMAs), so decode / head / store stay off the critical chain.
+    float z_pend = 0.0f;
+    int64_t kk_pend = -1;
+    auto flush = [&]() {
+      if (kk_pend < 0) return;
+      int r, tx, ty;
+      decode(first + kk_pend * tile_stride, r, tx, ty);
+      const int ix = kX3TX * tx + (wtid % kX3TX);
+      const int row = kX3TY * ty + (wtid / kX3TX);
+      const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
+      if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {
+        const float o = head_exact(a.m.head, z_pend);
+        if (t.out16) {
+          const __half ho = __float2half_rn(o);
+          t.out16[(int64_t)r * t.ld_out + (v - a.v0)] = *reinterpret_cast<const uint16_t*>(&ho);
+        } else {
+          a.out[v - a.v0] = o;
+        }
+      }
+      kk_pend = -1;
+    };
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
 #pragma unroll 1
@@ -709,9 +750,11 @@ query_x3_kernel(const TcArgs t) {
         tc_fence_after();
         if (l == 0 && lead && lane == 0) mbar_arrive(&s_free[s]);   // slot SMEM reusable
         if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 5 + 2 * l);
+        NDF_X3_TRACE_W(0);
         float va[16], vb[16];
         tmem_ld16_nowait(d_base + first_col, va);
         tmem_wait_ld();
+        NDF_X3_TRACE_W(1);
         if (l + 1 < H) {
 #ifdef NDF_EXP_X3_NOEPI      // timing experiment: hidden epilogues only signal (wrong results)
 #pragma unroll
@@ -731,10 +774,12 @@ query_x3_kernel(const TcArgs t) {
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             named_bar_arrive(1 + 4 * s + i, 288);
+            NDF_X3_TRACE_W(2 + i);
             if (i + 1 < 4) tmem_wait_ld();
           }
 #endif
           if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
+          if (l == 0) flush();
         } else {
           if (lead && lane == 0) mbar_arrive(&d_free[s]);
           float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -752,36 +797,31 @@ query_x3_kernel(const TcArgs t) {
           }
           tc_fence_before();
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
-          if (ch == 1) dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] = part;
-          named_bar(9 + s, 256);
-          if (ch == 0) {
-            int r, tx, ty;
-            decode(first + kk * tile_stride, r, tx, ty);
-            const int ix = kX3TX * tx + (wtid % kX3TX);
-            const int row = kX3TY * ty + (wtid / kX3TX);
-            const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
-            const float z = part + dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] + bias_out;
-            if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {
-              const float o = head_exact(a.m.head, z);
-              if (t.out16) {
-                const __half ho = __float2half_rn(o);
-                t.out16[(int64_t)r * t.ld_out + (v - a.v0)] = *reinterpret_cast<const uint16_t*>(&ho);
-              } else {
-                a.out[v - a.v0] = o;
-              }
-            }
+          float* dx = dotx + ((kk & 1) * kPPSlots + s) * kTileM;
+          if (wq == 0 && lane == 0) NDF_X3_TRACE(s, (int)kk, 20 + ch);
+          if (ch == 1) {
+            // dotx is double-buffered by tile parity: the column-1 warps run ahead into the
+            // next tile (they cannot pass its hidden epilogues without the column-0 warps,
+            // which read this buffer first)
+            dx[wtid] = part;
+            named_bar_arrive(9 + s, 256);
+          } else {
+            named_bar(9 + s, 256);
+            z_pend = part + dx[wtid] + bias_out;
+            kk_pend = kk;
+            if (H == 1) flush();       // no later hidden epilogue to hide it behind
           }
-          // no second barrier: dotx is double-buffered by tile parity, so the column-1
-          // warps may run ahead into the next tile (they pass the next barrier only after
-          // the column-0 warps finished reading this buffer)
+          if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 22);
           if (lead && lane == 0) NDF_X3_TRACE(s, (int)kk, 6 + 2 * l);
         }
       }
     }
+    flush();
     (void)n;
   }
   tc_fence_before();
   __syncthreads();
+  NDF_X3_TRACE_CTA(1);
   tc_fence_after();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
