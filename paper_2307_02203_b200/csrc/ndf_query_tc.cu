@@ -1241,6 +1241,26 @@ query_pp_kernel(const TcArgs t) {
     const float bias_out = vecs[H * kHid];
     const uint32_t wout_addr = w_addr + lay.wout_off;
     uint32_t acc_ph = 0u;
+    // a finished tile's output is written late, after the next tile's first epilogue (the
+    // column-0 warps would wait on the layer-1 MMAs there anyway) -- as in query_x3_kernel
+    float z_pend = 0.0f;
+    int64_t kk_pend = -1;
+    auto flush = [&]() {
+      if (kk_pend < 0) return;
+      const int64_t tile_g = first + kk_pend * tile_stride;
+      const int64_t r = t.n_ref == 1 ? 0 : (int64_t)((uint32_t)tile_g / (uint32_t)n_vt);
+      const int64_t vloc = (tile_g - r * n_vt) * kTileM + wtid;
+      if (vloc < n) {
+        const float o = head_exact(a.m.head, z_pend);
+        if (t.out16) {
+          const __half ho = __float2half_rn(o);
+          t.out16[r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&ho);
+        } else {
+          a.out[vloc] = o;
+        }
+      }
+      kk_pend = -1;
+    };
 #pragma unroll 1
     for (int64_t kk = 0; kk < cnt; ++kk) {
 #pragma unroll 1
@@ -1275,6 +1295,7 @@ query_pp_kernel(const TcArgs t) {
           }
           NDF_TRACE_WARP(6);
           NDF_TRACE_AT((int)kk, 2 * l + 1);
+          if (l == 0) flush();
         } else {
           // ---- last hidden layer: A is free for the producer; fp32 output dot ---------
           // layer H-1's MMA has completed, so the other D half (which held layer H-2 and
@@ -1297,29 +1318,23 @@ query_pp_kernel(const TcArgs t) {
           }
           tc_fence_before();
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
-          if (ch == 1) dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] = part;
-          named_bar(9 + s, 256);
-          NDF_TRACE_AT((int)kk, 2 * l + 1);
-          if (ch == 0) {
-            const int64_t tile_g = first + kk * tile_stride;
-            const int64_t r = t.n_ref == 1 ? 0 : (int64_t)((uint32_t)tile_g / (uint32_t)n_vt);
-            const int64_t vloc = (tile_g - r * n_vt) * kTileM + wtid;
-            const float z = part + dotx[((kk & 1) * kPPSlots + s) * kTileM + wtid] + bias_out;
-            if (vloc < n) {
-              const float o = head_exact(a.m.head, z);
-              if (t.out16) {
-                const __half ho = __float2half_rn(o);
-                t.out16[r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&ho);
-              } else {
-                a.out[vloc] = o;
-              }
-            }
+          float* dx = dotx + ((kk & 1) * kPPSlots + s) * kTileM;
+          if (ch == 1) {
+            dx[wtid] = part;
+            named_bar_arrive(9 + s, 256);
+          } else {
+            named_bar(9 + s, 256);
+            z_pend = part + dx[wtid] + bias_out;
+            kk_pend = kk;
+            if (H == 1) flush();
           }
+          NDF_TRACE_AT((int)kk, 2 * l + 1);
           // no second barrier: dotx is double-buffered by tile parity (see x3)
           NDF_TRACE_AT((int)kk, 6);
         }
       }
     }
+    flush();
   }
   tc_fence_before();
   __syncthreads();
