@@ -28,6 +28,9 @@ constexpr int kKsgThreads = 256;
 #ifndef NDF_KSG_PNET
 #define NDF_KSG_PNET 1           // compare-vector insertion network (knn_scan)
 #endif
+#ifndef NDF_KSG_ONESCAN
+#define NDF_KSG_ONESCAN 1        // one knn_scan call site for both scan axes
+#endif
 
 struct KsgArgs {
   int mode;                   // 0 ref-vs-node-columns, 1 fp64 rows, 2 vertex-major pairs
@@ -434,7 +437,14 @@ ksg_kernel(const KsgArgs g) {
       // lower bound of eps; scan the axis whose strip at that radius is thinner
       const double lb = fmax(kth_gap_1d(sa, M, q, k), kth_gap_1d(sb, M, qb, k));
       const bool along_b = strip_count(sb, P, yi, lb) < strip_count(sa, P, xi, lb);
+#if NDF_KSG_ONESCAN
+      // one scan loop for both axes (operands selected per lane): lanes of a warp that
+      // chose different axes no longer run two loops one after the other
+      const double eps = knn_scan<KP1>(along_b ? sb : sa, along_b ? asb : bsa, M,
+                                       along_b ? qb : q);
+#else
       const double eps = along_b ? knn_scan<KP1>(sb, asb, M, qb) : knn_scan<KP1>(sa, bsa, M, q);
+#endif
       const int nx = lower_bound_lt(sa, P, dadd(xi, eps)) - upper_bound_le(sa, P, dsub(xi, eps)) - 1;
       const int ny = lower_bound_lt(sb, P, dadd(yi, eps)) - upper_bound_le(sb, P, dsub(yi, eps)) - 1;
       if (g.counts) {

@@ -3,11 +3,13 @@
 # travels with gpurun); load one with NDF_LIB_PATH=variants/lib_<name>.so -- the product
 # library is never overwritten.  Names: base, trace (schedule stamps), nomufu (see NDF_EXP_*
 # in ndf_query_tc.cu / ndf_query_x3.cuh), or a comma-separated list of -D flags.
+# SRC=ndf_ksg.cu (any csrc/*.cu) rebuilds that file instead of ndf_query_tc.cu.
 set -e
 cd "$(dirname "$0")/.."
 python -m paper_2307_02203_b200.build > /dev/null
 mkdir -p variants
-OBJS=$(ls build/obj/*.o | grep -v ndf_query_tc.o)
+SRC=${SRC:-ndf_query_tc.cu}
+OBJS=$(ls build/obj/*.o | grep -v "${SRC%.cu}.o")
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -I paper_2307_02203_b200/csrc"
 for v in "$@"; do
   case $v in
@@ -21,7 +23,7 @@ for v in "$@"; do
     *) D="$(echo $v | tr ',' ' ')";;        # e.g. -DNDF_MBAR_HINT=2000
   esac
   n=$(echo "$v" | tr -c 'a-zA-Z0-9_\n' '_')
-  $NV $D -c paper_2307_02203_b200/csrc/ndf_query_tc.cu -o variants/q_$n.o &
+  $NV $D -c paper_2307_02203_b200/csrc/$SRC -o variants/q_$n.o &
 done
 wait
 for v in "$@"; do
