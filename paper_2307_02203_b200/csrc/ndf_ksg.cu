@@ -28,6 +28,9 @@ constexpr int kKsgThreads = 256;
 #ifndef NDF_KSG_PNET
 #define NDF_KSG_PNET 1           // compare-vector insertion network (knn_scan)
 #endif
+#ifndef NDF_KSG_DYN
+#define NDF_KSG_DYN 1            // scans handed out per point from a CTA queue
+#endif
 #ifndef NDF_KSG_ONESCAN
 #define NDF_KSG_ONESCAN 1        // one knn_scan call site for both scan axes
 #endif
@@ -363,6 +366,7 @@ ksg_kernel(const KsgArgs g) {
   int* posa = pb + P;                                // original index -> a'-sorted position
   int* posb = posa + P;                              // original index -> b'-sorted position
   __shared__ int bad_flag;
+  __shared__ int work_next;                          // NDF_KSG_DYN scan queue
   const int k = KP1 - 1;
 
   for (int64_t p = blockIdx.x; p < g.n; p += gridDim.x) {
@@ -430,6 +434,90 @@ ksg_kernel(const KsgArgs g) {
     }
     __syncthreads();
     // ---- k-NN (exact, scanned along the sparser axis) + marginal counts ------------
+#if NDF_KSG_DYN
+    // (a) per point: the lower bound of eps and the scan axis (uniform work per point);
+    //     posa is free now and holds (axis << 30 | sorted position) per a'-position q
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      const int i = pa[q];
+      const int qb = posb[i];
+      const double xi = sa[q], yi = bsa[q];
+      const double lb = fmax(kth_gap_1d(sa, M, q, k), kth_gap_1d(sb, M, qb, k));
+      const bool along_b = strip_count(sb, P, yi, lb) < strip_count(sa, P, xi, lb);
+      posa[q] = along_b ? (qb | (1 << 30)) : q;
+    }
+    if (threadIdx.x == 0) work_next = 0;
+    __syncthreads();
+    // (b) the scans, points handed out one at a time from a CTA counter: a lane whose
+    //     point is done takes the next one, so a warp's lanes stay busy instead of
+    //     waiting for the longest of 32 fixed points; eps -> terms[q]
+    {
+      int q = atomicAdd(&work_next, 1);
+      const double* sx = sa;
+      const double* yx = bsa;
+      double xi = 0.0, yi = 0.0, dl = INFINITY, dr = INFINITY;
+      int l = 0, r = 0;
+      double top[KP1];
+      auto begin = [&]() {
+        const int info = posa[q];
+        const int pos = info & ((1 << 30) - 1);
+        const bool ab = (info >> 30) != 0;
+        sx = ab ? sb : sa;
+        yx = ab ? asb : bsa;
+        xi = sx[pos];
+        yi = yx[pos];
+        top[0] = 0.0;
+#pragma unroll
+        for (int t = 1; t < KP1; ++t) top[t] = INFINITY;
+        l = pos - 1;
+        r = pos + 1;
+        dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY;       // = |x_i - x_l| exactly
+        dr = r < M ? dsub(sx[r], xi) : INFINITY;
+      };
+      if (q < M) begin();
+      while (q < M) {
+        const bool left = dl <= dr;
+        const double dx = left ? dl : dr;
+        if (!(dx < top[KP1 - 1])) {                      // every j with d < eps visited
+          terms[q] = top[KP1 - 1];
+          q = atomicAdd(&work_next, 1);
+          if (q < M) begin();
+          continue;
+        }
+        const int j = left ? l : r;
+        const double d = fmax(dx, fabs(dsub(yi, yx[j])));
+        bool pl[KP1];                                    // insertion network as knn_scan
+#pragma unroll
+        for (int t = 1; t < KP1; ++t) pl[t] = d < top[t];
+#pragma unroll
+        for (int t = KP1 - 1; t > 1; --t) top[t] = pl[t - 1] ? top[t - 1] : (pl[t] ? d : top[t]);
+        top[1] = pl[1] ? d : top[1];
+        if (left) { --l; dl = l >= 0 ? dsub(xi, sx[l]) : INFINITY; }
+        else { ++r; dr = r < M ? dsub(sx[r], xi) : INFINITY; }
+      }
+    }
+    __syncthreads();
+    // (c) marginal counts per point; the psi terms go to ftm (posa / posb, free now) in
+    //     original order for the pairwise mean
+    double* ftm = reinterpret_cast<double*>(posa);
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      const int i = pa[q];
+      const double xi = sa[q], yi = bsa[q], eps = terms[q];
+      const int nx = lower_bound_lt(sa, P, dadd(xi, eps)) - upper_bound_le(sa, P, dsub(xi, eps)) - 1;
+      const int ny = lower_bound_lt(sb, P, dadd(yi, eps)) - upper_bound_le(sb, P, dsub(yi, eps)) - 1;
+      if (g.counts) {
+        g.counts[(p * 2) * (int64_t)M + i] = nx;
+        g.counts[(p * 2 + 1) * (int64_t)M + i] = ny;
+      }
+      if (nx < 0 || ny < 0) {
+        bad_flag = 1;
+        ftm[i] = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        ftm[i] = dadd(g.psi[nx], g.psi[ny]);
+      }
+    }
+    __syncthreads();
+    const double* tsum = ftm;
+#else
     for (int q = threadIdx.x; q < M; q += blockDim.x) {
       const int i = pa[q];
       const int qb = posb[i];
@@ -440,8 +528,12 @@ ksg_kernel(const KsgArgs g) {
 #if NDF_KSG_ONESCAN
       // one scan loop for both axes (operands selected per lane): lanes of a warp that
       // chose different axes no longer run two loops one after the other
+#ifdef NDF_EXP_KSG_NOSCAN   // timing experiment: eps = the lower bound (wrong results)
+      const double eps = lb + 0.0 * (double)along_b;
+#else
       const double eps = knn_scan<KP1>(along_b ? sb : sa, along_b ? asb : bsa, M,
                                        along_b ? qb : q);
+#endif
 #else
       const double eps = along_b ? knn_scan<KP1>(sb, asb, M, qb) : knn_scan<KP1>(sa, bsa, M, q);
 #endif
@@ -459,8 +551,10 @@ ksg_kernel(const KsgArgs g) {
       }
     }
     __syncthreads();
+    const double* tsum = terms;
+#endif
     if (threadIdx.x == 0) {
-      const double mean = ddiv(pairwise_sum(terms, M), (double)M);
+      const double mean = ddiv(pairwise_sum(tsum, M), (double)M);
       const double mi = dsub(g.psi_km, mean);
       if (g.mi) g.mi[p] = mi;
       if (g.mi_f32) g.mi_f32[p] = (float)mi;
