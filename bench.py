@@ -787,6 +787,23 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
                      f"x{spec.features_per_level}, encoders {spec.encoder_widths()}, decoder "
                      f"{spec.decoder_widths()}, {spec.merge} merge, snake_alt, linear head"}
     del outr, mref
+    # ---- the /api/reconstruct binary data plane (body + value-range
+    # headers in pinned host memory), host wall clock per call like e2e --------------------
+    if rank == 0:
+        for _ in range(args.warmup):
+            ndf.reconstruct_response(model, w.ref_position(), ndf.ROLE_MU, w.dims)
+        ts = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            resp = ndf.reconstruct_response(model, w.ref_position(), ndf.ROLE_MU, w.dims)
+            ts.append((time.perf_counter() - t0) * 1e3)
+            del resp
+        line["f4_response"] = {
+            "ms": statistics.mean(ts), "bytes": 4 * V,
+            "note": "reconstruct_response (service.py:392-410 without HTTP): query into HBM, "
+                    "then ndf_field_export writes the fp32 body to pinned host memory and "
+                    "reduces the X-Value-Min / X-Value-Max range in the same pass"}
     # ---- CPU baseline of the headline (rank 0, N=1 only): the full config-1 grid -------
     if cpu:
         m32 = model.with_precision("fp32")

@@ -226,6 +226,20 @@ int ndf_ksg_pairs(const float* Xv, int32_t M, int64_t V, const int64_t* pa,
                   const double* psi_tab, double psi_k_plus_psi_m, double* mi,
                   float* mi_f32, int32_t* counts, int32_t* status_out, void* stream);
 
+/* ---- binary data plane ------------------------------------------------------ */
+
+/* Body and value range of a field response -- /api/reconstruct and /api/diff
+ * (service.py:392-416: grid.values.astype("<f4").tobytes(), _field_headers at
+ * service.py:352-360).  dst[i] = a[i] (b == NULL) or a[i] - b[i] (fp32, difference_field,
+ * service.py:87-94), clipped to [-1, 1] when clamp (np.clip: NaN stays NaN), for
+ * i in [0, n); a / b on the device, dst device or page-locked host memory (the stores
+ * then go straight over PCIe).  stats (device, 3 x uint32) receives the min and max of
+ * the non-NaN values as order-preserving keys (key = bits ^ 0x80000000 for sign 0,
+ * ~bits for sign 1; min key 0xffffffff and max key 0 when there is none) and
+ * stats[2] = 1 if any value is NaN. */
+int ndf_field_export(const float* a, const float* b, int64_t n, float* dst, uint32_t* stats,
+                     int32_t clamp, void* stream);
+
 /* ---- utilities ------------------------------------------------------------ */
 
 /* Number of kernel launches this library issued on the calling thread since

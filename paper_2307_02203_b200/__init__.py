@@ -19,8 +19,9 @@ from .measures import (CorrelationMeasure, FieldGrid, digamma, gaussian_mi_analy
                        ksg_rows, load_field_grid, pair_estimators_device, pearson,
                        pearson_against, pearson_rowwise, save_field_grid)
 from .model import DeviceModel, ModelSpec, NdfModel, as_model, load_model, save_model
-from .service import (ROLE_MU, ROLE_NU, benchmark, difference_field, forward, matrix_reconstruct,
-                      reconstruct_field, reconstruct_field_device, reconstruct_multi_device)
+from .service import (ROLE_MU, ROLE_NU, FieldResponse, benchmark, difference_field,
+                      difference_response, forward, matrix_reconstruct, reconstruct_field,
+                      reconstruct_field_device, reconstruct_multi_device, reconstruct_response)
 
 __version__ = "0.1.0"
 
@@ -34,6 +35,7 @@ __all__ = [
     "load_ensemble_device",
     "load_field_grid", "load_model", "matrix_reconstruct", "pair_estimators_device", "pearson",
     "pearson_against", "pearson_rowwise", "reconstruct_field", "reconstruct_field_device",
-    "reconstruct_multi_device", "sample_at",
+    "reconstruct_multi_device", "sample_at", "FieldResponse", "reconstruct_response",
+    "difference_response",
     "sample_many", "save_ensemble", "save_field_grid", "save_model",
 ]

@@ -83,6 +83,7 @@ SIGNATURES = {
     "ndf_sample_many_ld": (ctypes.c_int, [_c_p, _i32, _i64, _i64, _i32, _i32, _i32, _c_p, _i64,
                                           _c_p, _c_p]),
     "ndf_pearson_field": (ctypes.c_int, [_c_p, _i32, _i64, _i64, _c_p, _i64, _i64, _c_p, _c_p]),
+    "ndf_field_export": (ctypes.c_int, [_c_p, _c_p, _i64, _c_p, _c_p, _i32, _c_p]),
     "ndf_zscore": (ctypes.c_int, [_c_p, _i32, _i64, _i64, _i64, _c_p, _c_p, _c_p]),
     "ndf_pearson_gemv": (ctypes.c_int, [_c_p, _c_p, _i32, _i64, _c_p, _i32, _i64, _i64, _c_p,
                                         _c_p]),

@@ -2,7 +2,9 @@
 
 ``reconstruct_field`` (service.py:46-84), ``difference_field`` (:87-94),
 ``matrix_reconstruct`` (:97-125) and ``benchmark`` (:186-220) with the
-reference's signatures.  The query runs as ONE kernel launch over the whole
+reference's signatures, plus the binary data plane of ``/api/reconstruct`` and
+``/api/diff`` (:392-416) without the HTTP layer: ``reconstruct_response`` /
+``difference_response``.  The query runs as ONE kernel launch over the whole
 output grid: the reference point is embedded once per CTA, every query vertex
 once, and the decoder runs fused on the tensor cores (fp16 / bf16 models) or in
 exact fp32 (fp32 models).  ``batch_size`` is accepted for signature compatibility;
@@ -141,11 +143,90 @@ def to_host(t) -> np.ndarray:
 
 def difference_field(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,
                      batch_size: int = DEFAULT_QUERY_BATCH) -> FieldGrid:
-    """service.py:87-94."""
+    """service.py:87-94 -- reconstruct(ref_a) - reconstruct(ref_b), elementwise (fp32)."""
+    return difference_response(model, ref_a, ref_b, dims, role, batch_size).grid()
+
+
+# ---- binary data plane (/api/reconstruct, /api/diff without the HTTP layer) ----------
+
+@dataclass
+class FieldResponse:
+    """What ``/api/reconstruct`` and ``/api/diff`` send (service.py:392-396): the field as
+    little-endian fp32 bytes (x fastest) and the ``_field_headers`` of service.py:352-360.
+    ``body`` is a zero-copy view of the page-locked buffer the export kernel wrote;
+    ``content()`` is the ``bytes`` an HTTP layer would send."""
+    dims: tuple
+    body: memoryview
+    headers: dict
+    media_type: str = "application/octet-stream"
+    _values: np.ndarray | None = None
+
+    def content(self) -> bytes:
+        return bytes(self.body)
+
+    def grid(self) -> FieldGrid:
+        return FieldGrid(self.dims, self._values)
+
+
+def _key_to_float(key: int) -> float:
+    bits = key ^ 0x80000000 if key & 0x80000000 else (~key) & 0xFFFFFFFF
+    return float(np.array([bits], dtype=np.uint32).view(np.float32)[0])
+
+
+def _export(dims, fa, fb, clamp: bool) -> FieldResponse:
+    """One ndf_field_export launch: body (a or a - b, clipped if clamp) into pinned host
+    memory plus the min / max keys; one stream sync."""
+    import torch
+    V = dims[0] * dims[1] * dims[2]
+    host = torch.empty(V, dtype=torch.float32, pin_memory=True)
+    stats = torch.empty(3, dtype=torch.int32, device=fa.device)
+    stream = torch.cuda.current_stream(fa.device)
+    N.call("ndf_field_export", fa.data_ptr(), 0 if fb is None else fb.data_ptr(), V,
+           host.data_ptr(), stats.data_ptr(), 1 if clamp else 0, stream.cuda_stream)
+    st = stats.cpu().numpy().view(np.uint32)          # syncs the stream
+    values = host.numpy()
+    if V == 0:
+        lo = hi = 0.0
+    elif st[2]:
+        lo = hi = float("nan")                        # np.min / np.max propagate NaN
+    else:
+        lo, hi = _key_to_float(int(st[0])), _key_to_float(int(st[1]))
+    return FieldResponse(dims, memoryview(values).cast("B"), field_headers(dims, lo, hi),
+                         _values=values)
+
+
+def field_headers(dims, lo: float, hi: float) -> dict:
+    """``_field_headers`` (service.py:352-360) from the value range."""
+    x, y, z = dims
+    return {"X-Dims": f"{x},{y},{z}", "X-Value-Min": repr(float(lo)),
+            "X-Value-Max": repr(float(hi))}
+
+
+def reconstruct_response(model: NdfModel, ref, role: str = ROLE_MU, dims=(64, 64, 64),
+                         batch_size: int = DEFAULT_QUERY_BATCH,
+                         clamp: bool = False) -> FieldResponse:
+    """``/api/reconstruct`` (service.py:406-410 + ``_binary`` :392-396): the query into
+    HBM, then one export kernel writes the body into pinned host memory and reduces
+    the header's value range (``reconstruct_field``'s clamp fused into it)."""
+    _check_role(role)
     model = as_model(model)
+    if batch_size < 1:
+        raise ParameterError("batch_size must be >= 1")
+    dims = _check_dims(dims)
+    fa = reconstruct_field_device(model, ref, role, dims)
+    return _export(dims, fa, None, clamp)
+
+
+def difference_response(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,
+                        batch_size: int = DEFAULT_QUERY_BATCH) -> FieldResponse:
+    """``/api/diff`` (service.py:412-416): two queries into HBM, their fp32 difference
+    (difference_field, service.py:87-94) formed inside the export kernel."""
+    _check_role(role)
+    model = as_model(model)
+    dims = _check_dims(dims)
     fa = reconstruct_field_device(model, ref_a, role, dims)
     fb = reconstruct_field_device(model, ref_b, role, dims)
-    return FieldGrid(_check_dims(dims), (fa - fb).cpu().numpy())
+    return _export(dims, fa, fb, False)
 
 
 def matrix_reconstruct(models: list, variables: list, ref, dims,

@@ -90,3 +90,31 @@ def test_stand_in_objects_match_the_reference_structure(refndf):
     assert again.spec == ours.spec
     for x, y in zip(ours.parameters(), again.parameters()):
         assert np.array_equal(x, y)
+
+
+def _kernel_key(f32: np.ndarray) -> np.ndarray:
+    """The export kernel's order-preserving key (ndf_field_io.cu ordered_key), in NumPy."""
+    b = f32.astype(np.float32).view(np.uint32)
+    return np.where(b & 0x80000000, ~b, b | 0x80000000).astype(np.uint32)
+
+
+def test_response_headers_match_reference_field_headers(refndf):
+    """service.py:352-360 on the reference's own FieldGrid vs field_headers fed by the
+    kernel's min / max keys (decoded as service._key_to_float does)."""
+    from ndf import service as rservice
+    from ndf.measures import FieldGrid as RGrid
+    from paper_2307_02203_b200 import service as S
+    rng = np.random.default_rng(5)
+    cases = [rng.standard_normal(7 * 5 * 3).astype(np.float32),
+             np.array([-0.0, 0.0, 1e-45, -1e-45, 3.0], np.float32)[:5].repeat(3)[:15],
+             np.full(15, -2.5, np.float32)]
+    for vals in cases:
+        dims = (5, 3, 1) if vals.size == 15 else (7, 5, 3)
+        want = rservice._field_headers(RGrid(dims, vals))
+        keys = _kernel_key(vals)
+        got = S.field_headers(dims, S._key_to_float(int(keys.min())),
+                              S._key_to_float(int(keys.max())))
+        assert got == want
+    # order of the keys is the float order (sign flip / negative reversal)
+    x = np.sort(rng.standard_normal(1000).astype(np.float32))
+    assert np.all(np.diff(_kernel_key(x).astype(np.int64)) >= 0)
