@@ -435,14 +435,23 @@ ksg_kernel(const KsgArgs g) {
     __syncthreads();
     // ---- k-NN (exact, scanned along the sparser axis) + marginal counts ------------
 #if NDF_KSG_DYN
-    // (a) per point: the lower bound of eps and the scan axis (uniform work per point);
+    // (a) per point: the scan axis (uniform work per point);
     //     posa is free now and holds (axis << 30 | sorted position) per a'-position q
     for (int q = threadIdx.x; q < M; q += blockDim.x) {
       const int i = pa[q];
       const int qb = posb[i];
       const double xi = sa[q], yi = bsa[q];
+#ifndef NDF_KSG_STRIPAXIS
+      // the axis whose k-th 1-D gap is larger is locally sparser (fewer candidates per
+      // unit of radius); any choice gives the same eps -- this only steers the work.
+      // Measured +7% over counting both strips at the lower bound (4 binary searches).
+      const double ga = kth_gap_1d(sa, M, q, k), gb = kth_gap_1d(sb, M, qb, k);
+      const bool along_b = gb > ga;
+      (void)xi; (void)yi;
+#else
       const double lb = fmax(kth_gap_1d(sa, M, q, k), kth_gap_1d(sb, M, qb, k));
       const bool along_b = strip_count(sb, P, yi, lb) < strip_count(sa, P, xi, lb);
+#endif
       posa[q] = along_b ? (qb | (1 << 30)) : q;
     }
     if (threadIdx.x == 0) work_next = 0;
