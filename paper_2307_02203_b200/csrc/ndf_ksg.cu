@@ -24,7 +24,10 @@
 
 namespace ndf {
 
-constexpr int kKsgThreads = 256;
+#ifndef NDF_KSG_THREADS
+#define NDF_KSG_THREADS 256
+#endif
+constexpr int kKsgThreads = NDF_KSG_THREADS;
 #ifndef NDF_KSG_PNET
 #define NDF_KSG_PNET 1           // compare-vector insertion network (knn_scan)
 #endif
