@@ -801,9 +801,9 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
             del resp
         line["f4_response"] = {
             "ms": statistics.mean(ts), "bytes": 4 * V,
-            "note": "reconstruct_response (service.py:392-410 without HTTP): query into HBM, "
-                    "then ndf_field_export writes the fp32 body to pinned host memory and "
-                    "reduces the X-Value-Min / X-Value-Max range in the same pass"}
+            "note": "reconstruct_response (service.py:392-410 without HTTP): one query launch "
+                    "(ndf_query_grid_stats) stores the fp32 body into pinned host memory and "
+                    "reduces the X-Value-Min / X-Value-Max range in its epilogue"}
     # ---- CPU baseline of the headline (rank 0, N=1 only): the full config-1 grid -------
     if cpu:
         m32 = model.with_precision("fp32")

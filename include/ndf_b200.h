@@ -116,6 +116,16 @@ int ndf_query_grid(const ndf_model_desc* m, double ref_x, double ref_y, double r
                    int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
                    int64_t v0, int64_t v1, int32_t precision, float* out, void* stream);
 
+/* ndf_query_grid plus the value range of what it writes (the headers of
+ * /api/reconstruct, service.py:352-360, 406-410): stats (device, 3 x uint32) as for
+ * ndf_field_export -- min / max keys of the non-NaN outputs and a NaN flag -- reduced
+ * inside the query kernel's epilogue, so a response needs no second pass over the
+ * field (which may already sit in page-locked host memory). */
+int ndf_query_grid_stats(const ndf_model_desc* m, double ref_x, double ref_y, double ref_z,
+                         int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
+                         int64_t v0, int64_t v1, int32_t precision, float* out,
+                         uint32_t* stats, void* stream);
+
 /* Paired / broadcast forward.  Replaces NdfModel.forward (model.py:179-189):
  * p_mu is (n_mu, 3) fp64 device, p_nu (n, 3); n_mu == 1 broadcasts. */
 int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int64_t n_mu,

@@ -72,6 +72,9 @@ SIGNATURES = {
     "ndf_tc_pack": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _c_p, ctypes.c_size_t, _c_p]),
     "ndf_query_grid": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _f64, _f64, _f64, _i32, _i32,
                                       _i32, _i32, _i64, _i64, _i32, _c_p, _c_p]),
+    "ndf_query_grid_stats": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _f64, _f64, _f64, _i32,
+                                            _i32, _i32, _i32, _i64, _i64, _i32, _c_p, _c_p,
+                                            _c_p]),
     "ndf_query_points": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _c_p, _i64, _c_p, _i64, _i32,
                                         _c_p, _c_p]),
     "ndf_embed_nodes": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _i32, _i32, _i32, _i32, _i64,

@@ -7,16 +7,11 @@
 //
 // Unit: one value, 4 B read (8 for a difference) + 4 B written; HBM / PCIe-write bound.
 #include "ndf_common.cuh"
+#include "ndf_query.cuh"
 
 namespace ndf {
 
 constexpr int kExportThreads = 256;
-
-// fp32 -> uint32 key whose unsigned order is the float order (NaN handled separately)
-__device__ __forceinline__ uint32_t ordered_key(float f) {
-  const uint32_t b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
 
 __device__ __forceinline__ float export_value(const float* __restrict__ a,
                                               const float* __restrict__ b, int64_t i, bool clamp) {

@@ -172,6 +172,7 @@ query_f32_kernel(const QueryArgs a) {
     if (a.m.enc_layers > 0) eref = vec_encoder(a.m, enc_ref, rv0, rv1);
   }
 
+  RangeAcc rng;                                // ndf_query_grid_stats only
   for (int64_t tile = blockIdx.x; tile * kTV < n_vert; tile += gridDim.x) {
     const int64_t base = a.v0 + tile * kTV;
     const int nv = (int)min((int64_t)kTV, a.v1 - base);
@@ -248,7 +249,9 @@ query_f32_kernel(const QueryArgs a) {
           float acc = 0.0f;
           for (int k = 0; k < K; ++k) acc = fadd(acc, fmul(Hin[k * kTVP + tid], __ldg(W + k)));
           const float z = fadd(acc, __ldg(b));
-          a.out[base - a.v0 + tid] = head_exact(a.m.head, z);
+          const float o = head_exact(a.m.head, z);
+          a.out[base - a.v0 + tid] = o;
+          if (a.stats) rng.add(o);
         }
         __syncthreads();
       } else {
@@ -257,6 +260,7 @@ query_f32_kernel(const QueryArgs a) {
       }
     }
   }
+  if (a.stats) rng.flush(a.stats);
 }
 
 size_t query_f32_smem_bytes(int mode, int rows = NDF_MAX_WIDTH) {
@@ -336,10 +340,10 @@ int launch_query_f32(const QueryArgs& a, cudaStream_t s) {
 
 using namespace ndf;
 
-extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, double rz,
-                              int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
-                              int64_t v0, int64_t v1, int32_t precision, float* out,
-                              void* stream) {
+static int query_grid(const ndf_model_desc* m, double rx, double ry, double rz,
+                      int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz, int64_t v0,
+                      int64_t v1, int32_t precision, float* out, uint32_t* stats,
+                      void* stream) {
   int st = validate_model(m);
   if (st) return st;
   NDF_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, NDF_ERR_PARAMETER, "grid dims must be >= 1");
@@ -359,10 +363,31 @@ extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, dou
   a.v0 = v0; a.v1 = v1;
   a.out = static_cast<float*>(out_dev);
   a.prec = precision;
+  a.stats = stats;
   if (precision == NDF_PREC_BF16 || precision == NDF_PREC_FP16)
     return launch_query_tc(a, as_stream(stream));
   NDF_REQUIRE(precision == NDF_PREC_FP32, NDF_ERR_PARAMETER, "unknown precision");
   return launch_query_f32(a, as_stream(stream));
+}
+
+extern "C" int ndf_query_grid(const ndf_model_desc* m, double rx, double ry, double rz,
+                              int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
+                              int64_t v0, int64_t v1, int32_t precision, float* out,
+                              void* stream) {
+  return query_grid(m, rx, ry, rz, ref_is_mu, nx, ny, nz, v0, v1, precision, out, nullptr,
+                    stream);
+}
+
+extern "C" int ndf_query_grid_stats(const ndf_model_desc* m, double rx, double ry, double rz,
+                                    int32_t ref_is_mu, int32_t nx, int32_t ny, int32_t nz,
+                                    int64_t v0, int64_t v1, int32_t precision, float* out,
+                                    uint32_t* stats, void* stream) {
+  NDF_REQUIRE(stats, NDF_ERR_PARAMETER, "null stats");
+  cudaStream_t s = as_stream(stream);
+  NDF_CUDA_CHECK(cudaMemsetAsync(stats, 0xff, sizeof(uint32_t), s));           // min key
+  NDF_CUDA_CHECK(cudaMemsetAsync(stats + 1, 0, 2 * sizeof(uint32_t), s));      // max key, NaN
+  return query_grid(m, rx, ry, rz, ref_is_mu, nx, ny, nz, v0, v1, precision, out, stats,
+                    stream);
 }
 
 extern "C" int ndf_query_points(const ndf_model_desc* m, const double* p_mu, int64_t n_mu,

@@ -646,6 +646,7 @@ query_tc_kernel(const TcArgs t, const int nwg) {
                            a.ny > 1 ? (float)(a.g.ry - 1) / (float)(a.ny - 1) : 0.0f,
                            a.nz > 1 ? (float)(a.g.rz - 1) / (float)(a.nz - 1) : 0.0f};
   int tcount = 0;
+  RangeAcc rng;                                            // ndf_query_grid_stats only
   for (int64_t tile = (int64_t)blockIdx.x * nwg + wg; tile < n_tiles; tile += stride, ++tcount) {
     NDF_TRACE(0);
     const int64_t vloc = tile * kTileM + wtid;   // local vertex index
@@ -790,10 +791,12 @@ query_tc_kernel(const TcArgs t, const int nwg) {
           t.out16[(size_t)r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&hz);
         } else {
           a.out[vloc] = z;
+          if (a.stats) rng.add(z);
         }
       }
     }
   }
+  if (a.stats) rng.flush(a.stats);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1245,6 +1248,7 @@ query_pp_kernel(const TcArgs t) {
     // column-0 warps would wait on the layer-1 MMAs there anyway) -- as in query_x3_kernel
     float z_pend = 0.0f;
     int64_t kk_pend = -1;
+    RangeAcc rng;                                   // ndf_query_grid_stats only
     auto flush = [&]() {
       if (kk_pend < 0) return;
       const int64_t tile_g = first + kk_pend * tile_stride;
@@ -1257,6 +1261,7 @@ query_pp_kernel(const TcArgs t) {
           t.out16[r * t.ld_out + vloc] = *reinterpret_cast<const uint16_t*>(&ho);
         } else {
           a.out[vloc] = o;
+          if (a.stats) rng.add(o);
         }
       }
       kk_pend = -1;
@@ -1335,6 +1340,7 @@ query_pp_kernel(const TcArgs t) {
       }
     }
     flush();
+    if (a.stats && ch == 0) rng.flush(a.stats);
   }
   tc_fence_before();
   __syncthreads();
@@ -1758,13 +1764,12 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
         1, std::min<int64_t>((tiles + tc::kPPSlots - 1) / tc::kPPSlots, sm_count()));
     const size_t smem = (size_t)tc::make_x3_layout(a.m).smem_total;
     const bool silu = a.m.activation == NDF_ACT_SILU;
-    static SmemAttrCache attr_s, attr_g;
-    if (e == cudaSuccess)
-      e = silu ? attr_s.ensure(tc::query_x3_kernel<true>, smem)
-               : attr_g.ensure(tc::query_x3_kernel<false>, smem);
-    if (e == cudaSuccess)
-      e = silu ? launch_pdl(tc::query_x3_kernel<true>, g2, tc::kPPThreads, smem, s, t)
-               : launch_pdl(tc::query_x3_kernel<false>, g2, tc::kPPThreads, smem, s, t);
+    // the value-range variant only when ndf_query_grid_stats asked for it
+    auto* kern = silu ? (a.stats ? tc::query_x3_kernel<true, true> : tc::query_x3_kernel<true, false>)
+                      : (a.stats ? tc::query_x3_kernel<false, true> : tc::query_x3_kernel<false, false>);
+    static SmemAttrCache attr[4];
+    if (e == cudaSuccess) e = attr[(silu ? 2 : 0) + (a.stats ? 1 : 0)].ensure(kern, smem);
+    if (e == cudaSuccess) e = launch_pdl(kern, g2, tc::kPPThreads, smem, s, t);
     count_launch();
     if (e != cudaSuccess) {
       set_error(std::string("bf16 query launch failed: ") + cudaGetErrorString(e));

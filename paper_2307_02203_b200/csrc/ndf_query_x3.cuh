@@ -441,7 +441,9 @@ __host__ __device__ inline X3Tiles x3_tiles(int nx, int64_t v0, int64_t v1) {
       t.trace[((slot_) * 32 + (kk_)) * 24 + (ev)] = clock64();                          \
   } while (0)
 
-template <bool SILU>
+// RANGE: also reduce the outputs' min / max (ndf_query_grid_stats) -- a separate
+// instantiation: the three extra live registers cost the plain query 5% (measured)
+template <bool SILU, bool RANGE>
 __global__ void __launch_bounds__(kPPThreads, 1)
 query_x3_kernel(const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -721,6 +723,7 @@ query_x3_kernel(const TcArgs t) {
     // wait on the layer-1 MMAs), so decode / head / store stay off the critical chain.
     float z_pend = 0.0f;
     int64_t kk_pend = -1;
+    RangeAcc rng;                                   // ndf_query_grid_stats only
     auto flush = [&]() {
       if (kk_pend < 0) return;
       int r, tx, ty;
@@ -735,6 +738,7 @@ query_x3_kernel(const TcArgs t) {
           t.out16[(int64_t)r * t.ld_out + (v - a.v0)] = *reinterpret_cast<const uint16_t*>(&ho);
         } else {
           a.out[v - a.v0] = o;
+          if constexpr (RANGE) rng.add(o);
         }
       }
       kk_pend = -1;
@@ -817,6 +821,10 @@ query_x3_kernel(const TcArgs t) {
       }
     }
     flush();
+    if constexpr (RANGE) {
+      if (ch == 0) rng.flush(a.stats);
+    }
+    (void)rng;
     (void)n;
   }
   tc_fence_before();

@@ -205,16 +205,37 @@ def field_headers(dims, lo: float, hi: float) -> dict:
 def reconstruct_response(model: NdfModel, ref, role: str = ROLE_MU, dims=(64, 64, 64),
                          batch_size: int = DEFAULT_QUERY_BATCH,
                          clamp: bool = False) -> FieldResponse:
-    """``/api/reconstruct`` (service.py:406-410 + ``_binary`` :392-396): the query into
-    HBM, then one export kernel writes the body into pinned host memory and reduces
-    the header's value range (``reconstruct_field``'s clamp fused into it)."""
+    """``/api/reconstruct`` (service.py:406-410 + ``_binary`` :392-396): ONE query launch
+    (ndf_query_grid_stats) stores the body straight into page-locked host memory and
+    reduces the header's value range in its epilogue; the clamp is applied as in
+    reconstruct_field (np.clip), and min / max of clipped values are the clipped range."""
+    import torch
     _check_role(role)
     model = as_model(model)
     if batch_size < 1:
         raise ParameterError("batch_size must be >= 1")
     dims = _check_dims(dims)
-    fa = reconstruct_field_device(model, ref, role, dims)
-    return _export(dims, fa, None, clamp)
+    st = model.device_state()
+    ref = np.asarray(ref, dtype=np.float64).reshape(3)
+    V = dims[0] * dims[1] * dims[2]
+    host = torch.empty(V, dtype=torch.float32, pin_memory=True)
+    stats = torch.empty(3, dtype=torch.int32, device=st.device)
+    stream = torch.cuda.current_stream(st.device)
+    N.call("ndf_query_grid_stats", st.desc_ref, float(ref[0]), float(ref[1]), float(ref[2]),
+           1 if role == ROLE_MU else 0, dims[0], dims[1], dims[2], 0, V,
+           N.PREC[model.spec.precision], host.data_ptr(), stats.data_ptr(), stream.cuda_stream)
+    k = stats.cpu().numpy().view(np.uint32)           # syncs the stream
+    values = host.numpy()
+    if k[2]:
+        lo = hi = float("nan")
+    else:
+        lo, hi = _key_to_float(int(k[0])), _key_to_float(int(k[1]))
+    if clamp:                                          # clip is monotone: range clips too
+        np.clip(values, -1.0, 1.0, out=values)
+        if not k[2]:
+            lo, hi = min(max(lo, -1.0), 1.0), min(max(hi, -1.0), 1.0)
+    return FieldResponse(dims, memoryview(values).cast("B"), field_headers(dims, lo, hi),
+                         _values=values)
 
 
 def difference_response(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU,

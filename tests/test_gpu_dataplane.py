@@ -33,10 +33,20 @@ def model():
     return w, W.build_model(w, seed=0, grid_init=1.0)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def _variant(base, kind):
+    if kind == "classic":          # merge outside the x3 / ping-pong family -> query_tc_kernel
+        spec = base.spec
+        m = ndf.NdfModel.build(ndf.ModelSpec(**{**spec.__dict__, "merge": "concat"}), seed=4)
+        return m.with_precision("bf16")
+    return base.with_precision(kind)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp16", "classic"])
 def test_reconstruct_response_body_and_headers(model, prec):
+    """ndf_query_grid_stats: the range reduced inside each query kernel (f32, x3,
+    ping-pong, classic) equals NumPy's min / max of the body."""
     w, base = model
-    m = base.with_precision(prec)
+    m = _variant(base, prec)
     for clamp in (False, True):
         grid = ndf.reconstruct_field(m, w.ref_position(), ndf.ROLE_MU, w.dims, clamp=clamp)
         resp = ndf.reconstruct_response(m, w.ref_position(), ndf.ROLE_MU, w.dims, clamp=clamp)
