@@ -25,10 +25,19 @@ __device__ __forceinline__ void store_slab(const float* stage, int ld, int E, in
                                            float* __restrict__ dst) {
   const float invE = 1.0f / (float)E;
   const int total = rows * E;
-  for (int k = threadIdx.x; k < total; k += kEmbThreads) {
+  auto at = [&](int k) {
     const int r = (int)(((float)k + 0.5f) * invE);
-    dst[k] = stage[r * ld + (k - r * E)];
+    return stage[r * ld + (k - r * E)];
+  };
+  int k0 = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {      // 16-byte stores
+    const int t4 = total >> 2;
+    for (int q = threadIdx.x; q < t4; q += kEmbThreads)
+      reinterpret_cast<float4*>(dst)[q] = make_float4(at(4 * q), at(4 * q + 1), at(4 * q + 2),
+                                                      at(4 * q + 3));
+    k0 = 4 * t4;
   }
+  for (int k = k0 + threadIdx.x; k < total; k += kEmbThreads) dst[k] = at(k);
 }
 
 // mode 0: grid nodes [v0, v0 + n) of an nx x ny x nz output grid (x fastest,
@@ -39,7 +48,7 @@ embed_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int mode, in
              float* __restrict__ out) {
   extern __shared__ float stage[];
   const int E = g.E;
-  const int ld = E + 1;
+  const int ld = E | 1;            // odd row stride: the per-thread row writes hit 32 banks
   const float* grid = branch == 0 ? m.grid_mu : m.grid_nu;
   const int64_t base = (int64_t)blockIdx.x * kEmbThreads;
   const int64_t i = base + threadIdx.x;
@@ -102,12 +111,15 @@ __global__ void embed_axis_kernel(const EmbedGeom g, int nx, int ny, int nz, flo
   row[2 + 2 * o] = (float)cs;
 }
 
-__global__ void __launch_bounds__(kEmbThreads)
+#ifndef NDF_EMB_MINBLOCKS
+#define NDF_EMB_MINBLOCKS 6      // 80 registers: 6 CTAs per SM (measured best of 1 / 6 / 8 / 12)
+#endif
+__global__ void __launch_bounds__(kEmbThreads, NDF_EMB_MINBLOCKS)
 embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx, int ny, int nz,
                    int64_t v0, int64_t n, const float* __restrict__ tab, float* __restrict__ out) {
   extern __shared__ float stage[];
   const int E = g.E, L = g.L, C = g.C;
-  const int ld = E + 1;
+  const int ld = E | 1;            // odd row stride: the per-thread row writes hit 32 banks
   const float* grid = branch == 0 ? m.grid_mu : m.grid_nu;
   const int64_t base = (int64_t)blockIdx.x * kEmbThreads;
   const int64_t i = base + threadIdx.x;
@@ -121,13 +133,21 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
     const float* rows[3] = {tab + (size_t)ix * kAxisRowF, tab + (size_t)(nx + iy) * kAxisRowF,
                             tab + (size_t)(nx + ny + iz) * kAxisRowF};
     float* dst = stage + threadIdx.x * ld;
+    // axis rows: [p | sin_0, cos_0, ..., sin_{L-1}, cos_{L-1} | ...], 128-byte aligned:
+    // 16-byte loads of the first 4 (L + 1) / 4 quads, scattered into embed_point's order
+    // [p_xyz | (sin, cos)_x, (sin, cos)_y, (sin, cos)_z per octave]
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) dst[ax] = __ldg(rows[ax]);
-    for (int o = 0; o < L; ++o) {
+    for (int ax = 0; ax < 3; ++ax) {
+      const float4* r4 = reinterpret_cast<const float4*>(rows[ax]);
+      for (int q = 0; 4 * q < 1 + 2 * L; ++q) {
+        const float4 f = __ldg(r4 + q);
+        const float e4[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        dst[3 + 6 * o + 2 * ax] = __ldg(rows[ax] + 1 + 2 * o);
-        dst[3 + 6 * o + 2 * ax + 1] = __ldg(rows[ax] + 2 + 2 * o);
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;                  // position in the axis row
+          if (j == 0) dst[ax] = e4[u];
+          else if (j <= 2 * L) dst[3 + 6 * ((j - 1) >> 1) + 2 * ax + ((j - 1) & 1)] = e4[u];
+        }
       }
     }
     // latent: embed_point's corner order, weights ((wx) * wy) * wz and fp64 sums
