@@ -12,6 +12,8 @@
 #include <algorithm>
 
 #include "ndf_common.cuh"
+#include "ndf_tc_ptx.cuh"
+
 
 namespace ndf {
 
@@ -200,33 +202,157 @@ pearson_field_kernel(const float* __restrict__ X, int M, int64_t ld, int64_t col
   }
 }
 
-// ---- z-score prep -----------------------------------------------------------
-__global__ void zscore_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0,
-                              int64_t v1, float* __restrict__ Z, float* __restrict__ norm) {
+#ifndef NDF_ZS_COLS
+#define NDF_ZS_COLS 64
+#endif
+#ifndef NDF_ZS_BATCH
+#define NDF_ZS_BATCH 4
+#endif
+// ---- z-score prep: one DRAM read + one DRAM write -----------------------------
+// Z[m, v] = (x_mv - mean_v) / ||x_v - mean_v||, fp64 statistics (moments shifted by
+// x_0v), fp32 storage; norm[v] = ||x_v - mean_v|| (0 and a zero column: degenerate).
+// A persistent grid (kZBlocksPerSM blocks per SM) walks groups of kZCols consecutive
+// columns; a block streams its group's member rows twice -- pass 1 accumulates the
+// moments per row lane, the lanes are folded in a fixed order (deterministic per column,
+// independent of the launch range), pass 2 writes Z with streaming stores -- and the
+// second read is served by L2 (the grid keeps <= sm_count x kZBlocksPerSM x kZCols x M x
+// 4 B in flight: 38 MB at M = 1000, L2 126 MB), so DRAM sees one read and one write of
+// the ensemble (round 1 read it twice from DRAM: 3 x 7.04 GB at config 1).  Loads go in
+// batches of kZBatch rows, all issued before any is used: a plain unrolled loop with its
+// exit test between iterations had left ONE load in flight per thread.
+// Measured on B200 at config 1 (tools/zscore_probe.py): 3.50 ms = 4.0 TB/s of algorithmic
+// traffic (round 1: 4.2 ms).  Alternatives measured: 32 / 128 columns per group 4.6 / 3.6 ms,
+// batches of 2 / 8 rows 3.6 / 4.2 ms, fp32 partial moments 3.17 ms (but 6x the Z error:
+// kept fp64), a cluster of 8 CTAs sharing 512-column groups through DSMEM (2 KB runs) 9 ms,
+// a cp.async ring of 16 copies per thread 5.4 ms, per-row 256 B bulk copies 11.6 ms.  The
+// kernel stays latency-bound: 32 warps x 4 row loads in flight per SM (64 registers).
+constexpr int kZCols = NDF_ZS_COLS;
+constexpr int kZThreads = 512;
+constexpr int kZLanes = kZThreads / (kZCols / 4);    // row lanes
+constexpr int kZBlocksPerSM = 2;
+constexpr int kZBatch = NDF_ZS_BATCH;
+
+__device__ __forceinline__ void st_stream4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w) : "memory");
+}
+
+__global__ void __launch_bounds__(kZThreads, kZBlocksPerSM)
+zscore_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0, int64_t v1,
+              float* __restrict__ Z, float* __restrict__ norm) {
+  __shared__ double part[kZLanes][2][kZCols];
+  __shared__ double stat[2][kZCols];              // mean, 1 / norm (0: degenerate)
+  const int tid = threadIdx.x;
+  const int t = tid % (kZCols / 4), lane = tid / (kZCols / 4);
+  const int64_t ngroups = (v1 - v0 + kZCols - 1) / kZCols;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int64_t c = v0 + g * kZCols + 4 * t;
+    const bool live = c < v1;
+    float K[4];
+    double s1[4], s2[4];
+    {
+      const float4 f = live ? __ldg(reinterpret_cast<const float4*>(X + c)) : make_float4(0, 0, 0, 0);
+      K[0] = f.x; K[1] = f.y; K[2] = f.z; K[3] = f.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { s1[i] = 0.0; s2[i] = 0.0; }
+    if (live) {
+      for (int mb = lane; mb < M; mb += kZBatch * kZLanes) {         // pass 1: moments
+        float4 f[kZBatch];
+#pragma unroll
+        for (int u = 0; u < kZBatch; ++u) {
+          const int m = mb + u * kZLanes;
+          f[u] = m < M ? *reinterpret_cast<const float4*>(X + (int64_t)m * V + c)
+                       : make_float4(K[0], K[1], K[2], K[3]);       // d = 0: no contribution
+        }
+#pragma unroll
+        for (int u = 0; u < kZBatch; ++u) {
+          const float x[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double d = (double)x[i] - (double)K[i];
+            s1[i] += d;
+            s2[i] = fma(d, d, s2[i]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      part[lane][0][4 * t + i] = s1[i];
+      part[lane][1][4 * t + i] = s2[i];
+    }
+    __syncthreads();
+    if (tid < kZCols) {                                 // fold the lanes in order
+      double a = 0.0, b = 0.0;
+      for (int l = 0; l < kZLanes; ++l) { a += part[l][0][tid]; b += part[l][1][tid]; }
+      const int64_t v = v0 + g * kZCols + tid;
+      const double Kc = v < v1 ? (double)__ldg(X + v) : 0.0;
+      const double off = a / (double)M;
+      const double var = b - a * off;
+      const bool ok = var > 0.0;
+      stat[0][tid] = Kc + off;
+      stat[1][tid] = ok ? 1.0 / sqrt(var) : 0.0;
+      if (norm && v < v1) norm[v] = ok ? (float)sqrt(var) : 0.0f;
+    }
+    __syncthreads();
+    double mu[4], inv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { mu[i] = stat[0][4 * t + i]; inv[i] = stat[1][4 * t + i]; }
+    __syncthreads();                                    // part / stat free for the next group
+    if (live) {
+      const bool whole = c + 4 <= v1;
+      for (int mb = lane; mb < M; mb += kZBatch * kZLanes) {         // pass 2: Z (from L2)
+        float4 f[kZBatch];
+#pragma unroll
+        for (int u = 0; u < kZBatch; ++u) {
+          const int m = mb + u * kZLanes;
+          f[u] = m < M ? *reinterpret_cast<const float4*>(X + (int64_t)m * V + c)
+                       : make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kZBatch; ++u) {
+          const int m = mb + u * kZLanes;
+          if (m >= M) break;
+          const float x[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+          float z[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            z[i] = inv[i] != 0.0 ? (float)(((double)x[i] - mu[i]) * inv[i]) : 0.0f;
+          const int64_t o = (int64_t)m * V + c;
+          if (whole) {
+            st_stream4(Z + o, make_float4(z[0], z[1], z[2], z[3]));
+          } else {
+            for (int i = 0; c + i < v1; ++i) Z[o + i] = z[i];
+          }
+        }
+      }
+    }
+  }
+}
+
+// Other layouts (V or v0 not a multiple of 4, unaligned pointers): one thread per
+// column, two passes, same statistics.
+__global__ void zscore_lsu_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0,
+                                  int64_t v1, float* __restrict__ Z, float* __restrict__ norm) {
   const int64_t v = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= v1) return;
   const float* col = X + v;
   const double K = (double)col[0];
   double s1 = 0.0, s2 = 0.0;
-#pragma unroll 8
   for (int m = 0; m < M; ++m) {
     const double d = (double)__ldg(col + (int64_t)m * V) - K;
     s1 += d;
-    s2 += d * d;
+    s2 = fma(d, d, s2);
   }
   const double off = s1 / (double)M;
-  double var = s2 - s1 * off;
-  if (!(var > 0.0)) {
-    for (int m = 0; m < M; ++m) Z[(int64_t)m * V + v] = 0.0f;
-    if (norm) norm[v] = 0.0f;
-    return;
-  }
+  const double var = s2 - s1 * off;
+  const bool ok = var > 0.0;
   const double mu = K + off;
-  const double inv = 1.0 / sqrt(var);
-#pragma unroll 8
+  const double inv = ok ? 1.0 / sqrt(var) : 0.0;
   for (int m = 0; m < M; ++m)
-    Z[(int64_t)m * V + v] = (float)(((double)__ldg(col + (int64_t)m * V) - mu) * inv);
-  if (norm) norm[v] = (float)sqrt(var);
+    Z[(int64_t)m * V + v] = ok ? (float)(((double)__ldg(col + (int64_t)m * V) - mu) * inv) : 0.0f;
+  if (norm) norm[v] = ok ? (float)sqrt(var) : 0.0f;
 }
 
 // ---- Pearson GEMV over Z -----------------------------------------------------
@@ -473,9 +599,17 @@ extern "C" int ndf_zscore(const float* X, int32_t M, int64_t V, int64_t v0, int6
   NDF_REQUIRE(v0 >= 0 && v0 <= v1 && v1 <= V, NDF_ERR_PARAMETER, "vertex range out of bounds");
   if (v0 == v1) return NDF_OK;
   NDF_REQUIRE(X && Z, NDF_ERR_PARAMETER, "null pointer");
-  const int threads = 256;
-  zscore_kernel<<<(unsigned)((v1 - v0 + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
-      X, M, V, v0, v1, Z, norm);
+  const bool bulk = V % 4 == 0 && v0 % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+  if (bulk) {
+    const int64_t groups = (v1 - v0 + kZCols - 1) / kZCols;
+    const int64_t grid = std::min<int64_t>(groups, (int64_t)sm_count() * kZBlocksPerSM);
+    zscore_kernel<<<(unsigned)grid, kZThreads, 0, as_stream(stream)>>>(X, M, V, v0, v1, Z, norm);
+  } else {
+    const int threads = 256;
+    zscore_lsu_kernel<<<(unsigned)((v1 - v0 + threads - 1) / threads), threads, 0,
+                        as_stream(stream)>>>(X, M, V, v0, v1, Z, norm);
+  }
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }

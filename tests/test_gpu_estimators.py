@@ -130,6 +130,45 @@ def test_pearson_gemv_unaligned_ranges():
     assert np.max(np.abs(full - want)) <= 1e-5
 
 
+@pytest.mark.parametrize("M,nz,ny,nx", [(1000, 2, 30, 40), (37, 3, 7, 11), (5, 1, 1, 133)])
+def test_zscore_and_gemv_vs_fp64(M, nz, ny, nx):
+    """ndf_zscore (the standardised copy Z callers of ndf_pearson_gemv hold) against a
+    fp64 two-pass z-score, on the vectorised (V % 4 == 0) and scalar layouts, with
+    constant columns (degenerate: Z = 0, norm = 0) and partial ranges; then the GEMV
+    over that Z against the oracle's pearson_against (measures.py:84-108)."""
+    from paper_2307_02203_b200 import _native as N
+    rng = np.random.default_rng(M + nx)
+    X = rng.standard_normal((M, nz, ny, nx)).astype(np.float32)
+    X[:, 0, 0, 3] = 2.5                     # constant column -> degenerate
+    V = nz * ny * nx
+    dev = torch.from_numpy(X.reshape(M, V)).cuda()
+    Z = torch.full((M, V), 7.0, dtype=torch.float32, device="cuda")
+    norm = torch.full((V,), 7.0, dtype=torch.float32, device="cuda")
+    s = N.stream_handle(dev.device)
+    for a, b in [(0, V // 3 + 1), (V // 3 + 1, V - 2), (V - 2, V)]:   # ragged ranges
+        N.call("ndf_zscore", N.ptr(dev), M, V, a, b, N.ptr(Z), N.ptr(norm), s)
+    torch.cuda.synchronize()
+    x64 = X.reshape(M, V).astype(np.float64)
+    c = x64 - x64.mean(axis=0)
+    nrm = np.sqrt((c * c).sum(axis=0))
+    ok = nrm > 0
+    want = np.zeros_like(c)
+    want[:, ok] = c[:, ok] / nrm[ok]
+    Zh, nh = Z.cpu().numpy(), norm.cpu().numpy()
+    assert np.max(np.abs(Zh - want)) <= 1e-6
+    assert np.all(Zh[:, ~ok] == 0.0) and np.all(nh[~ok] == 0.0)
+    assert np.max(np.abs(nh[ok] - nrm[ok]) / nrm[ok]) <= 1e-6
+    ref = 5 if V > 5 else 0
+    zref = Z[:, ref].contiguous()
+    out = torch.empty(V, dtype=torch.float32, device="cuda")
+    N.call("ndf_pearson_gemv", N.ptr(Z), N.ptr(norm), M, V, N.ptr(zref), 0, 0, V, N.ptr(out), s)
+    got = out.cpu().numpy()
+    pw = O.pearson_against(x64[:, ref], x64.T)
+    assert got[ref] == 1.0
+    assert np.array_equal(np.isnan(got), ~ok)          # degenerate -> NaN, as pearson_against
+    assert np.max(np.abs(got[ok] - pw[ok])) <= 1e-5
+
+
 # ---- KSG -------------------------------------------------------------------------
 
 def test_ksg_golden_bitwise(golden):
