@@ -502,6 +502,74 @@ __global__ void pearson_pairs_kernel(const float* __restrict__ Xv, int M,
   }
 }
 
+// Rows of M <= 128 * kPairNV members with M % 4 == 0: both rows are loaded ONCE into
+// registers (up to 2 x kPairNV 16-byte loads in flight per lane, all issued before any
+// is used) and both passes run from registers -- one read of 8 KB per pair at M = 1000
+// (the scalar two-pass kernel above re-read the rows and kept one load in flight).
+constexpr int kPairNV = 8;
+__global__ void __launch_bounds__(256)
+pearson_pairs_reg_kernel(const float* __restrict__ Xv, int M, const int64_t* __restrict__ pa,
+                         const int64_t* __restrict__ pb, int64_t n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n) return;
+  const float4* ar = reinterpret_cast<const float4*>(Xv + pa[p] * (int64_t)M);
+  const float4* br = reinterpret_cast<const float4*>(Xv + pb[p] * (int64_t)M);
+  const int n4 = M >> 2;
+  float4 a[kPairNV], b[kPairNV];
+#pragma unroll
+  for (int u = 0; u < kPairNV; ++u) {
+    const int i = lane + 32 * u;
+    a[u] = i < n4 ? __ldg(ar + i) : make_float4(0, 0, 0, 0);
+    b[u] = i < n4 ? __ldg(br + i) : make_float4(0, 0, 0, 0);
+  }
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int u = 0; u < kPairNV; ++u) {       // zero padding adds nothing
+    sa += ((double)a[u].x + (double)a[u].y) + ((double)a[u].z + (double)a[u].w);
+    sb += ((double)b[u].x + (double)b[u].y) + ((double)b[u].z + (double)b[u].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  const double ma = sa / M, mb = sb / M;
+  double saa = 0.0, sbb = 0.0, sab = 0.0;
+  int eq = 1;
+#pragma unroll
+  for (int u = 0; u < kPairNV; ++u) {
+    if (lane + 32 * u >= n4) break;
+    const float av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+    const float bv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double x = (double)av[q] - ma, y = (double)bv[q] - mb;
+      saa = fma(x, x, saa);
+      sbb = fma(y, y, sbb);
+      sab = fma(x, y, sab);
+      eq &= (av[q] == bv[q]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    saa += __shfl_xor_sync(0xffffffffu, saa, o);
+    sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+    sab += __shfl_xor_sync(0xffffffffu, sab, o);
+  }
+  eq = __all_sync(0xffffffffu, eq);
+  if (lane == 0) {
+    double r;
+    if (!(saa > 0.0) || !(sbb > 0.0)) {
+      r = __longlong_as_double(0x7ff8000000000000ll);   // degenerate (measures.py:94-100)
+    } else {
+      r = fmin(1.0, fmax(-1.0, sab / sqrt(saa * sbb)));
+      if (eq && r > 1.0 - 1e-9) r = 1.0;                // measures.py:128-131
+    }
+    out[p] = r;
+  }
+}
+
 // ---- member-major -> vertex-major transpose (K5) -----------------------------
 __global__ void transpose_kernel(const float* __restrict__ X, int M, int64_t V,
                                  float* __restrict__ Xv) {
@@ -656,8 +724,11 @@ extern "C" int ndf_pearson_pairs(const float* Xv, int32_t M, int64_t V, const in
   if (n == 0) return NDF_OK;
   NDF_REQUIRE(Xv && pa && pb && out, NDF_ERR_PARAMETER, "null pointer");
   const int threads = 256;
-  pearson_pairs_kernel<<<(unsigned)((n * 32 + threads - 1) / threads), threads, 0,
-                         as_stream(stream)>>>(Xv, M, pa, pb, n, out);
+  const unsigned blocks = (unsigned)((n * 32 + threads - 1) / threads);
+  if (M % 4 == 0 && M <= 128 * kPairNV && (reinterpret_cast<uintptr_t>(Xv) & 15) == 0)
+    pearson_pairs_reg_kernel<<<blocks, threads, 0, as_stream(stream)>>>(Xv, M, pa, pb, n, out);
+  else
+    pearson_pairs_kernel<<<blocks, threads, 0, as_stream(stream)>>>(Xv, M, pa, pb, n, out);
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }

@@ -261,6 +261,34 @@ def test_c2_shaped_ksg_field_subset_bitexact():
     assert np.array_equal(got[idx], want)
 
 
+@pytest.mark.parametrize("M", [2, 5, 301, 1000, 1024, 1100])
+def test_pearson_pairs_layouts(M):
+    """ndf_pearson_pairs on the register-resident path (M % 4 == 0, M <= 1024) and the
+    two-pass fallback, with a self pair (1.0), a constant row (NaN, measures.py:124-126)
+    and an affine copy, against the oracle's pearson_rowwise."""
+    from paper_2307_02203_b200 import _native as N
+    rng = np.random.default_rng(M)
+    V, n = 40, 64
+    Xv = rng.standard_normal((V, M)).astype(np.float32)
+    Xv[3] = 1.5                                   # constant row
+    Xv[4] = Xv[5] * 2.0 + 0.25                    # affine (r ~ 1, not forced)
+    pa = rng.integers(0, V, n)
+    pb = rng.integers(0, V, n)
+    pa[:4] = [7, 3, 4, 9]
+    pb[:4] = [7, 8, 5, 3]
+    dev = torch.from_numpy(Xv).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    tpa, tpb = torch.from_numpy(pa).cuda(), torch.from_numpy(pb).cuda()   # kept alive
+    N.call("ndf_pearson_pairs", N.ptr(dev), M, V, N.ptr(tpa), N.ptr(tpb), n, N.ptr(out),
+           N.stream_handle())
+    got = out.cpu().numpy()
+    want = O.pearson_rowwise(Xv[pa].astype(np.float64), Xv[pb].astype(np.float64))
+    assert got[0] == 1.0
+    assert np.array_equal(np.isnan(got), np.isnan(want)) and np.isnan(got[1]) and np.isnan(got[3])
+    ok = ~np.isnan(want)
+    assert np.max(np.abs(got[ok] - want[ok])) <= 1e-12
+
+
 def test_pairs_pearson_and_ksg_vs_oracle():
     rng = np.random.default_rng(21)
     grids = rng.standard_normal((300, 4, 6, 8)).astype(np.float32)
