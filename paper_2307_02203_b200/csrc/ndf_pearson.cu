@@ -208,6 +208,9 @@ pearson_field_kernel(const float* __restrict__ X, int M, int64_t ld, int64_t col
 #ifndef NDF_ZS_BATCH
 #define NDF_ZS_BATCH 4
 #endif
+#ifndef NDF_ZS_HINT
+#define NDF_ZS_HINT true
+#endif
 // ---- z-score prep: one DRAM read + one DRAM write -----------------------------
 // Z[m, v] = (x_mv - mean_v) / ||x_v - mean_v||, fp64 statistics (moments shifted by
 // x_0v), fp32 storage; norm[v] = ||x_v - mean_v|| (0 and a zero column: degenerate).
@@ -220,17 +223,40 @@ pearson_field_kernel(const float* __restrict__ X, int M, int64_t ld, int64_t col
 // the ensemble (round 1 read it twice from DRAM: 3 x 7.04 GB at config 1).  Loads go in
 // batches of kZBatch rows, all issued before any is used: a plain unrolled loop with its
 // exit test between iterations had left ONE load in flight per thread.
-// Measured on B200 at config 1 (tools/zscore_probe.py): 3.50 ms = 4.0 TB/s of algorithmic
-// traffic (round 1: 4.2 ms).  Alternatives measured: 32 / 128 columns per group 4.6 / 3.6 ms,
-// batches of 2 / 8 rows 3.6 / 4.2 ms, fp32 partial moments 3.17 ms (but 6x the Z error:
-// kept fp64), a cluster of 8 CTAs sharing 512-column groups through DSMEM (2 KB runs) 9 ms,
-// a cp.async ring of 16 copies per thread 5.4 ms, per-row 256 B bulk copies 11.6 ms.  The
+// The rows are read with L2 eviction-priority hints: evict_last in pass 1 (they must
+// survive until pass 2), evict_first in pass 2 -- without them 5.4 GB of the second read
+// still came from DRAM (the group footprint, 2 blocks x 148 SMs x 256 KB = 76 MB, shares
+// L2 with the 7 GB of streamed Z stores).  Measured on B200 at config 1
+// (tools/zscore_probe.py): 2.86 ms = 4.9 TB/s of algorithmic traffic, 0.75 of the copy
+// peak (round 1: 4.2 ms; this kernel without the hints 3.50 ms).  Alternatives measured:
+// 32 / 128 columns per group 4.5 / 3.2 ms, batches of 2 / 6 rows 3.26 / 2.85 ms, fp32
+// partial moments 3.17 ms without hints (6x the Z error: kept fp64), a cluster of 8 CTAs
+// sharing 512-column groups through DSMEM 9 ms, a cp.async ring of 16 copies per thread
+// 5.4 ms, per-row 256 B bulk copies 11.6 ms.  The
 // kernel stays latency-bound: 32 warps x 4 row loads in flight per SM (64 registers).
 constexpr int kZCols = NDF_ZS_COLS;
 constexpr int kZThreads = 512;
 constexpr int kZLanes = kZThreads / (kZCols / 4);    // row lanes
 constexpr int kZBlocksPerSM = 2;
 constexpr int kZBatch = NDF_ZS_BATCH;
+
+// 16-byte load with an L2 eviction-priority policy (createpolicy): pass 1 marks the
+// group's rows evict_last so they survive until pass 2, which reads them evict_first
+template <bool kLast>
+__device__ __forceinline__ float4 ld_l2hint4(const float* p) {
+  float4 r;
+  if constexpr (kLast)
+    asm volatile("{\n\t.reg .b64 pol;\n\t"
+                 "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                 "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  else
+    asm volatile("{\n\t.reg .b64 pol;\n\t"
+                 "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                 "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
 
 __device__ __forceinline__ void st_stream4(float* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
@@ -262,7 +288,7 @@ zscore_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0, int64_t
 #pragma unroll
         for (int u = 0; u < kZBatch; ++u) {
           const int m = mb + u * kZLanes;
-          f[u] = m < M ? *reinterpret_cast<const float4*>(X + (int64_t)m * V + c)
+          f[u] = m < M ? ld_l2hint4<NDF_ZS_HINT>(X + (int64_t)m * V + c)
                        : make_float4(K[0], K[1], K[2], K[3]);       // d = 0: no contribution
         }
 #pragma unroll
@@ -307,7 +333,7 @@ zscore_kernel(const float* __restrict__ X, int M, int64_t V, int64_t v0, int64_t
 #pragma unroll
         for (int u = 0; u < kZBatch; ++u) {
           const int m = mb + u * kZLanes;
-          f[u] = m < M ? *reinterpret_cast<const float4*>(X + (int64_t)m * V + c)
+          f[u] = m < M ? ld_l2hint4<false>(X + (int64_t)m * V + c)
                        : make_float4(0, 0, 0, 0);
         }
 #pragma unroll

@@ -2,7 +2,7 @@
 # Round profiling in parts (gpurun brings back <= 64 MiB of gpurun_out/ per call):
 #   bash tools/profile_round.sh bench   -- full bench, reference arm, launch list
 #   bash tools/profile_round.sh ncu1    -- ncu --set full: query_x3 (with source), prep, embed
-#   bash tools/profile_round.sh ncu2    -- ncu --set full: Pearson field, KSG, pair kernels
+#   bash tools/profile_round.sh ncu2    -- ncu --set full: Pearson field, KSG, pair kernels, z-score
 #   bash tools/profile_round.sh ncu3    -- ncu --set full: config-3 cube launch, fp16 query_pp
 # Each probe first runs plain and must exit 0.  Summarise here with
 # tools/summarize_profiles.py <round> gpurun_out/prof_*.ncu-rep.
@@ -34,7 +34,8 @@ case "${1:-bench}" in
     prof field pearson_field "" python tools/gemv_probe.py
     prof ksg ksg_kernel "" python tools/ksg_probe.py 16384
     prof pairs_ksg ksg_kernel "" python tools/c4_probe.py 16384
-    prof pairs_pearson pearson_pairs "" python tools/c4_probe.py 16384;;
+    prof pairs_pearson pearson_pairs "" python tools/pairs_pearson_probe.py
+    prof zscore zscore_kernel "" python tools/zscore_probe.py 1;;
   ncu3)
     prof c3 query_x3 "" python tools/c3_probe.py
     export PREC=fp16
