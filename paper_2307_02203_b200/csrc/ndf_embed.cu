@@ -11,6 +11,8 @@
 // SMEM ([point][E + 1], odd stride against bank conflicts) and written back as one
 // contiguous (128 x E) fp32 slab, so the stores are coalesced.  Grid nodes of dense-latent
 // models take the separable per-axis route (embed_nodes_kernel below).
+#include <algorithm>
+
 #include "ndf_query.cuh"
 
 namespace ndf {
@@ -29,15 +31,41 @@ __device__ __forceinline__ void store_slab(const float* stage, int ld, int E, in
     const int r = (int)(((float)k + 0.5f) * invE);
     return stage[r * ld + (k - r * E)];
   };
-  int k0 = 0;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {      // 16-byte stores
-    const int t4 = total >> 2;
-    for (int q = threadIdx.x; q < t4; q += kEmbThreads)
-      reinterpret_cast<float4*>(dst)[q] = make_float4(at(4 * q), at(4 * q + 1), at(4 * q + 2),
-                                                      at(4 * q + 3));
-    k0 = 4 * t4;
-  }
-  for (int k = k0 + threadIdx.x; k < total; k += kEmbThreads) dst[k] = at(k);
+  // scalar head up to the first 16-byte boundary, 16-byte stores, scalar tail
+  const int head = min(total, (int)(((16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u) >> 2));
+  if ((int)threadIdx.x < head) dst[threadIdx.x] = at(threadIdx.x);
+  const int t4 = (total - head) >> 2;
+  float4* d4 = reinterpret_cast<float4*>(dst + head);
+  for (int q = threadIdx.x; q < t4; q += kEmbThreads)
+    d4[q] = make_float4(at(head + 4 * q), at(head + 4 * q + 1), at(head + 4 * q + 2),
+                        at(head + 4 * q + 3));
+  for (int k = head + 4 * t4 + threadIdx.x; k < total; k += kEmbThreads) dst[k] = at(k);
+}
+
+// Odd E (ld == E): the staged rows ARE the slab in order, so when the rows start at
+// stage + slab_off(dst) the 16-byte stores read their 4 values with one aligned LDS.128
+// (the generic store_slab's 4 scalar reads per float4 hit 4-way bank conflicts).
+__device__ __forceinline__ int slab_head(const float* dst) {
+  return (int)(((16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u) >> 2);
+}
+__device__ __forceinline__ int slab_off(const float* dst) { return (4 - slab_head(dst)) & 3; }
+__device__ __forceinline__ void store_slab_lin(const float* lin, int total, float* __restrict__ dst) {
+  const int head = min(total, slab_head(dst));
+  if ((int)threadIdx.x < head) dst[threadIdx.x] = lin[threadIdx.x];
+  const int t4 = (total - head) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(lin + head);
+  float4* d4 = reinterpret_cast<float4*>(dst + head);
+  for (int q = threadIdx.x; q < t4; q += kEmbThreads) d4[q] = s4[q];
+  for (int k = head + 4 * t4 + threadIdx.x; k < total; k += kEmbThreads) dst[k] = lin[k];
+}
+// stage rows (ld floats apart) at stage_base(stage, ld, E, dst), then store_rows
+__device__ __forceinline__ float* stage_base(float* stage, int ld, int E, const float* dst) {
+  return ld == E ? stage + slab_off(dst) : stage;
+}
+__device__ __forceinline__ void store_rows(const float* base, int ld, int E, int rows,
+                                           float* __restrict__ dst) {
+  if (ld == E) store_slab_lin(base, rows * E, dst);
+  else store_slab(base, ld, E, rows, dst);
 }
 
 // mode 0: grid nodes [v0, v0 + n) of an nx x ny x nz output grid (x fastest,
@@ -69,11 +97,12 @@ embed_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int mode, in
       p[1] = pos[3 * i + 1];
       p[2] = pos[3 * i + 2];
     }
-    float* row = stage + threadIdx.x * ld;
+    float* row = stage_base(stage, ld, E, out + base * E) + threadIdx.x * ld;
     embed_point(g, grid, p[0], p[1], p[2], [&](int k, float x) { row[k] = x; });
   }
   __syncthreads();
-  store_slab(stage, ld, E, (int)min((int64_t)kEmbThreads, n - base), out + base * E);
+  store_rows(stage_base(stage, ld, E, out + base * E), ld, E,
+             (int)min((int64_t)kEmbThreads, n - base), out + base * E);
 }
 
 // ---- grid nodes of a dense-latent model: separable per axis ----------------------
@@ -132,7 +161,7 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
     const int ix = (int)(r - (int64_t)iy * nx);
     const float* rows[3] = {tab + (size_t)ix * kAxisRowF, tab + (size_t)(nx + iy) * kAxisRowF,
                             tab + (size_t)(nx + ny + iz) * kAxisRowF};
-    float* dst = stage + threadIdx.x * ld;
+    float* dst = stage_base(stage, ld, E, out + base * E) + threadIdx.x * ld;
     // axis rows: [p | sin_0, cos_0, ..., sin_{L-1}, cos_{L-1} | ...], 128-byte aligned:
     // 16-byte loads of the first 4 (L + 1) / 4 quads, scattered into embed_point's order
     // [p_xyz | (sin, cos)_x, (sin, cos)_y, (sin, cos)_z per octave]
@@ -201,7 +230,8 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
     }
   }
   __syncthreads();
-  store_slab(stage, ld, E, (int)min((int64_t)kEmbThreads, n - base), out + base * E);
+  store_rows(stage_base(stage, ld, E, out + base * E), ld, E,
+             (int)min((int64_t)kEmbThreads, n - base), out + base * E);
 }
 
 static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int nx, int ny, int nz,
@@ -215,12 +245,12 @@ static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int n
   void* out_dev = nullptr;
   if ((st = resolve_output(out, &out_dev))) return st;
   const EmbedGeom g = make_geom(*m);
-  const size_t smem = (size_t)kEmbThreads * (g.E + 1) * sizeof(float);
+  const size_t smem = ((size_t)kEmbThreads * (g.E + 1) + 4) * sizeof(float);
   if (mode == 0 && g.levels == 0) {
     // dense-latent model over grid nodes: per-axis tables, then table reads + latent sum
     static SmemAttrCache attr_n;
     NDF_CUDA_CHECK(attr_n.ensure(embed_nodes_kernel,
-                                 (size_t)kEmbThreads * (kMaxEmbed + 1) * sizeof(float)));
+                                 ((size_t)kEmbThreads * (kMaxEmbed + 1) + 4) * sizeof(float)));
     const int nodes = nx + ny + nz;
     void* tab = nullptr;
     NDF_CUDA_CHECK(scratch_alloc(&tab, (size_t)nodes * kAxisRowF * sizeof(float),
@@ -243,7 +273,7 @@ static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int n
     return NDF_OK;
   }
   static SmemAttrCache attr;
-  NDF_CUDA_CHECK(attr.ensure(embed_kernel, (size_t)kEmbThreads * (kMaxEmbed + 1) * sizeof(float)));
+  NDF_CUDA_CHECK(attr.ensure(embed_kernel, ((size_t)kEmbThreads * (kMaxEmbed + 1) + 4) * sizeof(float)));
   embed_kernel<<<(unsigned)((n + kEmbThreads - 1) / kEmbThreads), kEmbThreads, smem,
                  as_stream(stream)>>>(*m, g, branch, mode, nx, ny, nz, v0, pos, n,
                                       static_cast<float*>(out_dev));

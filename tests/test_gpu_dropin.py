@@ -97,3 +97,24 @@ def test_embed_bitwise_vs_oracle():
     with pytest.raises(ndf.ParameterError):
         m1.embed(np.zeros_like(m1.grid_mu), pts)
     assert m1.embed("mu", np.zeros((0, 3))).shape == (0, 55)
+
+
+def test_embed_nodes_row_segments_vs_oracle():
+    """embed_rows_kernel (fp64 corners staged per row segment): bit-exact over whole grids,
+    ragged ranges (odd starts: unaligned slabs), single-node axes and rows of several
+    128-node segments."""
+    from paper_2307_02203_b200.model import ModelSpec, NdfModel
+    cases = [((32, 44, 4), (4, 6, 2), None),            # config 0, whole grid
+             ((300, 5, 3), (75, 2, 2), (1, 1499)),      # 3 segments per row, odd ends
+             ((1, 7, 5), (2, 2, 2), None),              # nx = 1
+             ((130, 3, 1), (40, 2, 2), (127, 261)),     # latent finer along x than 1/4
+             ((250, 352, 20), (63, 88, 5), (1_759_001, 1_760_000))]
+    for dims, res, rng in cases:
+        spec = ModelSpec(measure_kind="pearson", grid_resolution=res, precision="fp32", grid_init=1.0)
+        m = NdfModel.build(spec, seed=3)
+        V = dims[0] * dims[1] * dims[2]
+        v0, v1 = rng if rng else (0, V)
+        for branch, table in (("mu", m.grid_mu), ("nu", m.grid_nu)):
+            got = m.embed_nodes(branch, dims, v0, v1).cpu().numpy()
+            want = O.embed(O.grid_positions_of(dims, np.arange(v0, v1)), table, 6)
+            assert np.array_equal(got, want), (dims, branch)
