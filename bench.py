@@ -638,7 +638,10 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
             "traffic": load_traffic().get("pearson_field_kernel"),
             "note": "one streaming read of X (fp64 shifted moments per column); what "
                     "ground_truth_field(pearson) runs on node-aligned grids",
-            "fresh_public_call_ms": fresh_ms, "members": M, "vertices": v1 - v0}
+            "fresh_public_call_ms": fresh_ms, "members": M, "vertices": v1 - v0,
+            "roofline": {"bound": "hbm", "achieved": fgbs, "peak": hbm, "unit": "GB/s",
+                         "frac": fgbs / hbm, "traffic": load_traffic().get("pearson_field_kernel"),
+                         "bytes_basis": "4 M B read + 4 B written per vertex column"}}
         line["pearson_gemv"] = {
             "ms": gms, "bytes": gbytes, "achieved_gbs": gemv_gbs, "peak_gbs": hbm,
             "frac": gemv_gbs / hbm, "peak_kind": f"{peak_kind} hbm copy",
@@ -647,7 +650,10 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
             "zscore_frac": zbytes / (zscore_ms * 1e-3) / 1e9 / hbm,
             "fresh_ensemble_ms": fresh_ms,
             "fresh_note": "public ground_truth_field_device on an ensemble with no cached Z",
-            "members": M, "vertices": v1 - v0}
+            "members": M, "vertices": v1 - v0,
+            "roofline": {"bound": "hbm", "achieved": gemv_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": gemv_gbs / hbm, "traffic": load_traffic().get("gemv_kernel"),
+                         "bytes_basis": "4 M B of Z read + 8 B per vertex (norm, out)"}}
     ens.drop_derived()
     del ens
     torch.cuda.empty_cache()
@@ -689,6 +695,17 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
                       f"the reference algorithm) in {procs} processes ({kdt:.1f} s wall)"}
         ksg["cpu_pairs_per_s"] = rate
         ksg["speedup_vs_cpu"] = pairs_s / rate
+        ksg["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": procs, "kind": "port",
+                               "sample": ksg["same_sample"]["sample"]}
+    tr = load_traffic()
+    ksg["roofline"] = {"bound": "sm", "achieved": tr.get("ksg_kernel_sm_pct"), "peak": 100.0,
+                       "unit": "% SM throughput (ncu)",
+                       "frac": (tr.get("ksg_kernel_sm_pct") or 0.0) / 100.0 or None,
+                       "traffic": tr.get("ksg_kernel_16384_pairs"),
+                       "source": "profiles/r02/prof_ksg.txt (ncu --set full, 16,384 c2 pairs)",
+                       "note": "fp64 compare / select work (exact k-NN scans, bitonic sorts, binary "
+                               "searches): no FLOP or byte roofline applies; SM throughput is the "
+                               "north_star's KSG evidence"}
     if rank == 0:
         line["ksg_mi"] = ksg
     # ---- config 4: bulk estimator pairs (Pearson + KSG), the full 2^22 list ----------
@@ -729,6 +746,17 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
         c4l["speedup_vs_cpu"] = c4l["pairs_per_s"] / c4l["cpu_pairs_per_s"]
         c4l["cpu_sample"] = (f"{nc} seeded pairs of the list, oracle pearson_rowwise + ksg_mi "
                              f"(scipy cKDTree) in {procs} processes, {cdt:.1f} s wall")
+        c4l["cpu_baseline"] = {"value": nc / cdt, "unit": "pairs/s", "cores": procs, "kind": "port",
+                               "sample": c4l["cpu_sample"]}
+    tr = load_traffic()
+    c4l["roofline"] = {"bound": "sm", "achieved": tr.get("ksg_kernel_pairs_sm_pct"), "peak": 100.0,
+                       "unit": "% SM throughput (ncu)",
+                       "frac": (tr.get("ksg_kernel_pairs_sm_pct") or 0.0) / 100.0 or None,
+                       "kernel": "ndf::ksg_kernel<9> (pairs mode), ~99% of the step",
+                       "source": "profiles/r02/prof_pairs_ksg.txt (ncu --set full)",
+                       "pearson_pairs": {"bound": "hbm", "unit": "% of DRAM peak (ncu)",
+                                         "achieved": tr.get("pearson_pairs_dram_pct"),
+                                         "source": "profiles/r02/prof_pairs_pearson.txt"}}
     if rank == 0:
         line["c4_bulk_pairs"] = c4l
     ens2.drop_derived()
@@ -769,6 +797,23 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
                                              "sfu_floor_ms": sfu3, "sfu_frac": sfu3 / c3_ms},
                                 "output": "fp16 cube 64 x 1.76M per head"}
     del cube, models
+    # ---- SURVEY row A2 standalone: the positional encoder (K1) over the config-1 grid
+    # (NdfModel.embed_nodes -> ndf_embed_nodes); the query kernels fuse it ------------------
+    emb_ms = max_over_ranks(ev_ms(lambda: model.embed_nodes("mu", w.dims, v0, v1),
+                                  max(1, args.steps // 2)), world)
+    if rank == 0:
+        eb = 4.0 * 55 * (v1 - v0)
+        egbs = eb / (emb_ms * 1e-3) / 1e9
+        line["encoder_k1"] = {
+            "ms": emb_ms, "vertices": v1 - v0, "features": 55,
+            "roofline": {"bound": "hbm", "achieved": egbs, "peak": hbm, "unit": "GB/s",
+                         "frac": egbs / hbm, "traffic": load_traffic().get("embed_nodes_kernel"),
+                         "bytes_basis": "220 B of fp32 features written per node (the latent "
+                                        "grid, 1.8 MB, and the axis tables stay in L2)"},
+            "kernel": "ndf::embed_nodes_kernel (+ embed_axis_kernel)",
+            "note": "bit-identical to the reference's fp64 embed; L1-bound on the latent "
+                    "corner reads (profiles/r02/prof_embed.txt)"}
+    torch.cuda.empty_cache()
     # ---- the reference's own default architecture (HashGrid + encoder
     # MLPs, exact fp32 path) queried over the config-1 grid ------------------------------
     mref = ndf.NdfModel.build(ndf.ModelSpec.reference_default(), seed=0)
