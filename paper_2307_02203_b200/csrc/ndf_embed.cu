@@ -110,10 +110,32 @@ embed_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int mode, in
 // (raw p, Fourier sin / cos), and so do the latent cell (i0, t) per axis: an axis table
 // computed once per launch (one fp64 sincos per node x octave, the same operations as
 // embed_point -> the same bits) turns the node embedding into table reads plus the fp64
-// eight-corner latent sum -- so the launch is bound by writing the (V, E) output.
-constexpr int kAxisRowF = 32;       // [p | sin, cos x L (L <= 12) | pad | t (fp64) | i0]
+// eight-corner latent sum.  The table is feature-major ([feature][axis node], then t and
+// i0 per axis node), so a warp's 32 consecutive x-nodes read each feature as one
+// coalesced 128-byte row instead of 32 scattered table rows.
+struct AxisTab {
+  const float* f;      // [1 + 2L][nodes]: p, (sin, cos) per octave
+  const double* t;     // [nodes]
+  const int* i0;       // [nodes]
+  int nodes;
+};
 
-__global__ void embed_axis_kernel(const EmbedGeom g, int nx, int ny, int nz, float* __restrict__ tab) {
+__host__ __device__ inline size_t axis_tab_bytes(int L, int nodes) {
+  return (((size_t)(1 + 2 * L) * nodes * 4 + 15) & ~(size_t)15) + (size_t)nodes * 8 +
+         (size_t)nodes * 4;
+}
+__host__ __device__ inline AxisTab axis_tab(void* base, int L, int nodes) {
+  AxisTab T;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  T.f = reinterpret_cast<const float*>(p);
+  p += ((size_t)(1 + 2 * L) * nodes * 4 + 15) & ~(size_t)15;
+  T.t = reinterpret_cast<const double*>(p);
+  T.i0 = reinterpret_cast<const int*>(p + (size_t)nodes * 8);
+  T.nodes = nodes;
+  return T;
+}
+
+__global__ void embed_axis_kernel(const EmbedGeom g, int nx, int ny, int nz, AxisTab T) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
   const int nodes = nx + ny + nz;
   const int L = g.L;
@@ -124,71 +146,90 @@ __global__ void embed_axis_kernel(const EmbedGeom g, int nx, int ny, int nz, flo
   else if (node < nx + ny) { i = node - nx; n = ny; res = g.ry; }
   else { i = node - nx - ny; n = nz; res = g.rz; }
   const double p = fmin(fmax(node_coord(i, n), -1.0), 1.0);
-  float* row = tab + (size_t)node * kAxisRowF;
+  float* f = const_cast<float*>(T.f);
   if (o == L) {                       // raw coordinate and the latent cell of this axis
-    row[0] = (float)p;
+    f[node] = (float)p;
     const AxisCoord c = level_coord(p, res);
-    reinterpret_cast<double*>(row)[14] = c.t;      // floats 28-29
-    reinterpret_cast<int*>(row)[30] = c.i0;
+    const_cast<double*>(T.t)[node] = c.t;
+    const_cast<int*>(T.i0)[node] = c.i0;
     return;
   }
   double scale = 3.141592653589793;
   for (int k = 0; k < o; ++k) scale = scale * 2.0;
   double sn, cs;
   sincos(dmul(scale, p), &sn, &cs);
-  row[1 + 2 * o] = (float)sn;
-  row[2 + 2 * o] = (float)cs;
+  f[(size_t)(1 + 2 * o) * nodes + node] = (float)sn;
+  f[(size_t)(2 + 2 * o) * nodes + node] = (float)cs;
 }
 
+// Latent corners of a warp's 32 nodes: when they lie in one (y, z)-row, their x cells form
+// a short run [c_lo, c_lo + S); the warp copies the 4 (dy, dz) x S x 16 corner values once,
+// coalesced, into its own SMEM block (cell stride 20 floats: the lanes' 16-byte reads of
+// different cells fall into different bank groups) and every lane reads its 8 corners
+// from there -- instead of 32 scattered 16-byte global loads per node through L1, the
+// kernel's bound before (L1 94% busy).  Warps that cross a row, or a run longer than
+// kEmbCells, load their corners directly.
+constexpr int kEmbCells = 12;
+constexpr int kEmbCellStride = 20;
+constexpr int kEmbWarpLat = 4 * kEmbCells * kEmbCellStride;     // floats per warp
+
 #ifndef NDF_EMB_MINBLOCKS
-#define NDF_EMB_MINBLOCKS 6      // 80 registers: 6 CTAs per SM (measured best of 1 / 6 / 8 / 12)
+#define NDF_EMB_MINBLOCKS 5
 #endif
 __global__ void __launch_bounds__(kEmbThreads, NDF_EMB_MINBLOCKS)
 embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx, int ny, int nz,
-                   int64_t v0, int64_t n, const float* __restrict__ tab, float* __restrict__ out) {
-  extern __shared__ float stage[];
+                   int64_t v0, int64_t n, const AxisTab T, float* __restrict__ out) {
+  extern __shared__ __align__(16) float stage[];
   const int E = g.E, L = g.L, C = g.C;
   const int ld = E | 1;            // odd row stride: the per-thread row writes hit 32 banks
   const float* grid = branch == 0 ? m.grid_mu : m.grid_nu;
   const int64_t base = (int64_t)blockIdx.x * kEmbThreads;
   const int64_t i = base + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* latw = stage + ((kEmbThreads * ld + 4 + 3) & ~3) + warp * kEmbWarpLat;
+  const int64_t plane = (int64_t)nx * ny;
+  const int64_t vi = v0 + min(i, n - 1);
+  const int iz = (int)(vi / plane);
+  const int64_t rr = vi - (int64_t)iz * plane;
+  const int iy = (int)(rr / nx);
+  const int ix = (int)(rr - (int64_t)iy * nx);
+  const int nodes = T.nodes;
+  // one (y, z)-row for the whole warp, every lane a node of the launch?
+  const int64_t wlast = base + 32 * warp + 31;
+  const bool full = wlast < n;
+  const int row = iy + ny * iz;
+  const bool one_row = full && __shfl_sync(0xffffffffu, row, 0) == __shfl_sync(0xffffffffu, row, 31);
+  const int i0x = __ldg(T.i0 + ix);
+  const int c_lo = __shfl_sync(0xffffffffu, i0x, 0);
+  const int S = __shfl_sync(0xffffffffu, i0x, 31) + 2 - c_lo;
+  const int i0y = __ldg(T.i0 + nx + iy), i0z = __ldg(T.i0 + nx + ny + iz);
+  const bool staged = C == 16 && one_row && S <= kEmbCells;
+  if (staged) {
+    for (int it = lane; it < 16 * S; it += 32) {
+      const int combo = it / (4 * S), rem = it - combo * 4 * S;
+      const int cell = rem >> 2, q = rem & 3;
+      const int idx = (c_lo + cell) + g.rx * ((i0y + (combo & 1)) + g.ry * (i0z + (combo >> 1)));
+      const float4 f = __ldg(reinterpret_cast<const float4*>(grid + (size_t)idx * 16) + q);
+      *reinterpret_cast<float4*>(latw + (combo * S + cell) * kEmbCellStride + 4 * q) = f;
+    }
+    __syncwarp();
+  }
+  float* const sbase = stage_base(stage, ld, E, out + base * E);
   if (i < n) {
-    const int64_t v = v0 + i;
-    const int64_t plane = (int64_t)nx * ny;
-    const int iz = (int)(v / plane);
-    const int64_t r = v - (int64_t)iz * plane;
-    const int iy = (int)(r / nx);
-    const int ix = (int)(r - (int64_t)iy * nx);
-    const float* rows[3] = {tab + (size_t)ix * kAxisRowF, tab + (size_t)(nx + iy) * kAxisRowF,
-                            tab + (size_t)(nx + ny + iz) * kAxisRowF};
-    float* dst = stage_base(stage, ld, E, out + base * E) + threadIdx.x * ld;
-    // axis rows: [p | sin_0, cos_0, ..., sin_{L-1}, cos_{L-1} | ...], 128-byte aligned:
-    // 16-byte loads of the first 4 (L + 1) / 4 quads, scattered into embed_point's order
-    // [p_xyz | (sin, cos)_x, (sin, cos)_y, (sin, cos)_z per octave]
+    float* dst = sbase + threadIdx.x * ld;
+    const int an[3] = {ix, nx + iy, nx + ny + iz};
+    // [p_xyz | (sin, cos)_x, (sin, cos)_y, (sin, cos)_z per octave], feature-major reads
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const float4* r4 = reinterpret_cast<const float4*>(rows[ax]);
-      for (int q = 0; 4 * q < 1 + 2 * L; ++q) {
-        const float4 f = __ldg(r4 + q);
-        const float e4[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * q + u;                  // position in the axis row
-          if (j == 0) dst[ax] = e4[u];
-          else if (j <= 2 * L) dst[3 + 6 * ((j - 1) >> 1) + 2 * ax + ((j - 1) & 1)] = e4[u];
-        }
+      dst[ax] = __ldg(T.f + an[ax]);
+      for (int o = 0; o < L; ++o) {
+        dst[3 + 6 * o + 2 * ax] = __ldg(T.f + (size_t)(1 + 2 * o) * nodes + an[ax]);
+        dst[3 + 6 * o + 2 * ax + 1] = __ldg(T.f + (size_t)(2 + 2 * o) * nodes + an[ax]);
       }
     }
     // latent: embed_point's corner order, weights ((wx) * wy) * wz and fp64 sums
-    double tt[3];
-    int i0[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      tt[ax] = __ldg(reinterpret_cast<const double*>(rows[ax]) + 14);
-      i0[ax] = __ldg(reinterpret_cast<const int*>(rows[ax]) + 30);
-    }
+    const double tt[3] = {__ldg(T.t + an[0]), __ldg(T.t + an[1]), __ldg(T.t + an[2])};
     double w[8];
-    int idx[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
@@ -196,7 +237,6 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
       const double wy = dy ? tt[1] : dsub(1.0, tt[1]);
       const double wz = dz ? tt[2] : dsub(1.0, tt[2]);
       w[c] = dmul(dmul(wx, wy), wz);
-      idx[c] = (i0[0] + dx) + g.rx * ((i0[1] + dy) + g.ry * (i0[2] + dz));
     }
     const int lb = 3 + 6 * L;
     if (C == 16) {
@@ -207,10 +247,15 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
       for (int ch = 0; ch < 16; ++ch) acc[ch] = 0.0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const float4* rowp = reinterpret_cast<const float4*>(grid + (size_t)idx[c] * 16);
+        const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+        const float4* rowp =
+            staged ? reinterpret_cast<const float4*>(latw + ((c >> 1) * S + (i0x - c_lo + dx)) *
+                                                                kEmbCellStride)
+                   : reinterpret_cast<const float4*>(
+                         grid + (size_t)((i0x + dx) + g.rx * ((i0y + dy) + g.ry * (i0z + dz))) * 16);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 f = __ldg(rowp + q);
+          const float4 f = staged ? rowp[q] : __ldg(rowp + q);
           acc[4 * q + 0] = dadd(acc[4 * q + 0], dmul(w[c], (double)f.x));
           acc[4 * q + 1] = dadd(acc[4 * q + 1], dmul(w[c], (double)f.y));
           acc[4 * q + 2] = dadd(acc[4 * q + 2], dmul(w[c], (double)f.z));
@@ -220,6 +265,10 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
 #pragma unroll
       for (int ch = 0; ch < 16; ++ch) dst[lb + ch] = (float)acc[ch];
     } else {
+      int idx[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        idx[c] = (i0x + (c & 1)) + g.rx * ((i0y + ((c >> 1) & 1)) + g.ry * (i0z + (c >> 2)));
       for (int ch = 0; ch < C; ++ch) {
         double acc = 0.0;
 #pragma unroll
@@ -230,8 +279,7 @@ embed_nodes_kernel(const ndf_model_desc m, const EmbedGeom g, int branch, int nx
     }
   }
   __syncthreads();
-  store_rows(stage_base(stage, ld, E, out + base * E), ld, E,
-             (int)min((int64_t)kEmbThreads, n - base), out + base * E);
+  store_rows(sbase, ld, E, (int)min((int64_t)kEmbThreads, n - base), out + base * E);
 }
 
 static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int nx, int ny, int nz,
@@ -249,21 +297,23 @@ static int launch_embed(const ndf_model_desc* m, int32_t branch, int mode, int n
   if (mode == 0 && g.levels == 0) {
     // dense-latent model over grid nodes: per-axis tables, then table reads + latent sum
     static SmemAttrCache attr_n;
-    NDF_CUDA_CHECK(attr_n.ensure(embed_nodes_kernel,
-                                 ((size_t)kEmbThreads * (kMaxEmbed + 1) + 4) * sizeof(float)));
     const int nodes = nx + ny + nz;
     void* tab = nullptr;
-    NDF_CUDA_CHECK(scratch_alloc(&tab, (size_t)nodes * kAxisRowF * sizeof(float),
-                                 as_stream(stream)));
+    NDF_CUDA_CHECK(scratch_alloc(&tab, axis_tab_bytes(g.L, nodes), as_stream(stream)));
+    const AxisTab T = axis_tab(tab, g.L, nodes);
     const int items = nodes * (g.L + 1);
-    embed_axis_kernel<<<(items + 127) / 128, 128, 0, as_stream(stream)>>>(g, nx, ny, nz,
-                                                                          static_cast<float*>(tab));
+    embed_axis_kernel<<<(items + 127) / 128, 128, 0, as_stream(stream)>>>(g, nx, ny, nz, T);
     cudaError_t e = cudaGetLastError();
     count_launch();
+    const size_t smem_n = ((((size_t)kEmbThreads * (g.E | 1) + 4 + 3) & ~(size_t)3) +
+                           (size_t)4 * kEmbWarpLat) * sizeof(float);
+    if (e == cudaSuccess)
+      e = attr_n.ensure(embed_nodes_kernel,
+                        ((((size_t)kEmbThreads * (kMaxEmbed + 1) + 4 + 3) & ~(size_t)3) +
+                         (size_t)4 * kEmbWarpLat) * sizeof(float));
     if (e == cudaSuccess) {
-      embed_nodes_kernel<<<(unsigned)((n + kEmbThreads - 1) / kEmbThreads), kEmbThreads, smem,
-                           as_stream(stream)>>>(*m, g, branch, nx, ny, nz, v0, n,
-                                                static_cast<const float*>(tab),
+      embed_nodes_kernel<<<(unsigned)((n + kEmbThreads - 1) / kEmbThreads), kEmbThreads, smem_n,
+                           as_stream(stream)>>>(*m, g, branch, nx, ny, nz, v0, n, T,
                                                 static_cast<float*>(out_dev));
       e = cudaGetLastError();
       count_launch();
