@@ -50,7 +50,8 @@ __device__ __forceinline__ void tile_layer_v(const float* Hin, float* Hout, cons
     float acc[VPT];
 #pragma unroll
     for (int v = 0; v < VPT; ++v) acc[v] = 0.0f;
-    for (int k = 0; k < K; ++k) {
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {          // unrolled: several weight loads in flight
       const float w = __ldg(W + (size_t)k * N + j);
       const float4* hr = reinterpret_cast<const float4*>(Hin + k * kTVP + v0);
 #pragma unroll
