@@ -22,6 +22,7 @@ from .model import DeviceModel, ModelSpec, NdfModel, as_model, load_model, save_
 from .service import (ROLE_MU, ROLE_NU, FieldResponse, benchmark, difference_field,
                       difference_response, forward, matrix_reconstruct, reconstruct_field,
                       reconstruct_field_device, reconstruct_multi_device, reconstruct_response)
+from .training import sample_pairs_with_targets, targets, targets_device
 
 __version__ = "0.1.0"
 
@@ -38,4 +39,5 @@ __all__ = [
     "reconstruct_multi_device", "sample_at", "FieldResponse", "reconstruct_response",
     "difference_response",
     "sample_many", "save_ensemble", "save_field_grid", "save_model",
+    "sample_pairs_with_targets", "targets", "targets_device",
 ]

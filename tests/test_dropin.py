@@ -118,3 +118,43 @@ def test_response_headers_match_reference_field_headers(refndf):
     # order of the keys is the float order (sign flip / negative reversal)
     x = np.sort(rng.standard_normal(1000).astype(np.float32))
     assert np.all(np.diff(_kernel_key(x).astype(np.int64)) >= 0)
+
+
+def test_training_pair_draws_match_reference(refndf, monkeypatch):
+    """training.sample_pairs_with_targets (training.py:122-150): the same Generator calls in
+    the same order as the reference, the same resampling of non-finite targets -- checked
+    with one deterministic stand-in for the target computation on both sides (the GPU
+    targets themselves: tests/test_gpu_training.py)."""
+    sys.path.insert(0, REF_SRC)
+    try:
+        from ndf import training as rtraining
+    finally:
+        sys.path.remove(REF_SRC)
+    from paper_2307_02203_b200 import training as ours
+
+    class Cfg:
+        measure = ndf.CorrelationMeasure("pearson")
+        var_mu = var_nu = "v"
+
+    import types
+    field = types.SimpleNamespace(domain=ndf.GridDomain(9, 7, 3))    # _grid_pairs reads .domain
+
+    def fake(field_obj, measure, var_mu, var_nu, p_mu, p_nu):   # NaN for ~1/3 of the pairs
+        t = p_mu.sum(axis=1) - p_nu[:, 0]
+        return np.where(np.abs(t) > 1.2, np.nan, t)
+
+    monkeypatch.setattr(rtraining, "_targets", fake)
+    monkeypatch.setattr(ours, "targets", fake)
+    for on_grid in (False, True):
+        got = ours.sample_pairs_with_targets(field, Cfg, np.random.default_rng(11), 300, on_grid)
+        want = rtraining.sample_pairs_with_targets(field, Cfg, np.random.default_rng(11), 300,
+                                                   on_grid)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+    def never(field_obj, measure, var_mu, var_nu, p_mu, p_nu):
+        return np.full(len(p_mu), np.nan)
+
+    monkeypatch.setattr(ours, "targets", never)
+    with pytest.raises(ndf.DataError):
+        ours.sample_pairs_with_targets(field, Cfg, np.random.default_rng(1), 5)

@@ -1,0 +1,64 @@
+"""Training-target drop-in on the GPU (training.py:111-119): off-grid position pairs,
+samples kept in HBM, one Pearson / KSG launch per chunk -- vs the oracle's sample_many +
+pearson_rowwise / ksg_mi on the same positions."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2307_02203_b200 as ndf
+from oracle import ndf_oracle as O
+from paper_2307_02203_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def test_targets_vs_oracle():
+    w = W.CONFIGS[0]
+    field = W.generate_host(w)
+    grids = field.member_grids("v")
+    rng = np.random.default_rng(7)
+    p_mu = rng.uniform(-1.0, 1.0, (300, 3))
+    p_nu = rng.uniform(-1.0, 1.0, (300, 3))
+    p_nu[:20] = p_mu[:20]                     # identical pairs -> exactly 1.0
+    p_nu[20:40] = O.grid_positions(w.dims)[rng.integers(0, w.n_vertices, 20)]   # nodes
+    a = O.sample_many(grids, p_mu)
+    b = O.sample_many(grids, p_nu)
+    got = ndf.targets(field, ndf.CorrelationMeasure("pearson"), "v", "v", p_mu, p_nu)
+    want = O.pearson_rowwise(a, b)
+    assert got.dtype == np.float64 and got.shape == (300,)
+    assert np.max(np.abs(got - want)) <= 1e-12
+    assert np.all(got[:20] == 1.0)
+    for k in (3, 8):
+        got = ndf.targets(field, ndf.CorrelationMeasure("ksg_mi", ksg_k=k), "v", "v", p_mu, p_nu)
+        want = np.array([O.ksg_mi(a[i], b[i], k) for i in range(len(a))])
+        assert np.array_equal(got, want)
+    # chunking does not change a bit
+    from paper_2307_02203_b200.training import targets_device
+    m = ndf.CorrelationMeasure("ksg_mi", ksg_k=3)
+    whole = targets_device(field, m, "v", "v", p_mu, p_nu).cpu().numpy()
+    chunked = targets_device(field, m, "v", "v", p_mu, p_nu, chunk=37).cpu().numpy()
+    assert np.array_equal(whole, chunked)
+    assert ndf.targets(field, m, "v", "v", np.zeros((0, 3)), np.zeros((0, 3))).shape == (0,)
+    with pytest.raises(ndf.ParameterError):
+        ndf.targets(field, m, "v", "v", p_mu, p_nu[:5])
+
+
+def test_sample_pairs_with_targets_gpu():
+    w = W.CONFIGS[0]
+    field = W.generate_host(w)
+
+    class Cfg:
+        measure = ndf.CorrelationMeasure("ksg_mi", ksg_k=3)
+        var_mu = var_nu = "v"
+
+    p_mu, p_nu, t = ndf.sample_pairs_with_targets(field, Cfg, np.random.default_rng(3), 64,
+                                                  on_grid=True)
+    assert p_mu.shape == p_nu.shape == (64, 3) and np.all(np.isfinite(t))
+    grids = field.member_grids("v")
+    want = np.array([O.ksg_mi(x, y, 3) for x, y in zip(O.sample_many(grids, p_mu),
+                                                       O.sample_many(grids, p_nu))])
+    assert np.array_equal(t, want)
