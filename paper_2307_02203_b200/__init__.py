@@ -19,7 +19,8 @@ from .measures import (CorrelationMeasure, FieldGrid, digamma, gaussian_mi_analy
                        ksg_rows, load_field_grid, pair_estimators_device, pearson,
                        pearson_against, pearson_rowwise, save_field_grid)
 from .model import DeviceModel, ModelSpec, NdfModel, as_model, load_model, save_model
-from .service import (ROLE_MU, ROLE_NU, FieldResponse, benchmark, difference_field,
+from .service import (ROLE_MU, ROLE_NU, ComparisonResult, FieldResponse, benchmark,
+                      compare_to_ground_truth, difference_field, psnr,
                       difference_response, forward, matrix_reconstruct, reconstruct_field,
                       reconstruct_field_device, reconstruct_multi_device, reconstruct_response)
 from .training import sample_pairs_with_targets, targets, targets_device
@@ -40,4 +41,5 @@ __all__ = [
     "difference_response",
     "sample_many", "save_ensemble", "save_field_grid", "save_model",
     "sample_pairs_with_targets", "targets", "targets_device",
+    "ComparisonResult", "compare_to_ground_truth", "psnr",
 ]

@@ -250,6 +250,56 @@ def difference_response(model: NdfModel, ref_a, ref_b, dims, role: str = ROLE_MU
     return _export(dims, fa, fb, False)
 
 
+PSNR_CAP_DB = 200.0                 # training.py:30
+
+
+def psnr(predicted, truth, peak: float | None = None) -> float:
+    """training.py:162-180 -- 10 log10(peak^2 / MSE) in dB, capped at PSNR_CAP_DB; ``peak``
+    defaults to the truth's value range (floored at 1e-6); exact matches return the cap."""
+    predicted = np.asarray(predicted, dtype=np.float64).ravel()
+    truth = np.asarray(truth, dtype=np.float64).ravel()
+    if predicted.size == 0 or predicted.shape != truth.shape:
+        raise ParameterError("need equally sized, non-empty inputs")
+    if peak is None:
+        peak = max(float(np.ptp(truth)), 1e-6)
+    if not peak > 0:
+        raise ParameterError(f"peak must be positive, got {peak}")
+    mse = float(np.mean((predicted - truth) ** 2))
+    if mse == 0.0:
+        return PSNR_CAP_DB
+    return min(10.0 * np.log10(peak * peak / mse), PSNR_CAP_DB)
+
+
+@dataclass
+class ComparisonResult:
+    """service.py:128-132."""
+    psnr_db: float
+    max_abs_err: float
+    error_field: FieldGrid
+
+
+def compare_to_ground_truth(model: NdfModel, field_obj, measure: CorrelationMeasure, ref,
+                            dims, role: str = ROLE_MU, workers: int = 1) -> ComparisonResult:
+    """service.py:135-155 -- the NDF reconstruction against the direct estimator field on
+    the same grid (the paper's evaluation): both fields are computed on the GPU
+    (ground_truth_field: one streaming Pearson pass or the KSG kernel; reconstruct_field:
+    the query kernels), the error field and PSNR on the host as the reference does."""
+    _check_role(role)
+    model = as_model(model)
+    var_mu, var_nu = model.spec.var_mu, model.spec.var_nu
+    if role == ROLE_MU:
+        truth = ground_truth_field(field_obj, measure, var_mu, var_nu, ref, dims, workers=workers)
+    else:
+        truth = ground_truth_field(field_obj, measure, var_nu, var_mu, ref, dims, workers=workers)
+    recon = reconstruct_field(model, ref, role, dims)
+    err = recon.values.astype(np.float64) - truth.values.astype(np.float64)
+    return ComparisonResult(
+        psnr_db=psnr(recon.values, truth.values),
+        max_abs_err=float(np.max(np.abs(err))) if err.size else 0.0,
+        error_field=FieldGrid(dims, err.astype(np.float32)),
+    )
+
+
 def matrix_reconstruct(models: list, variables: list, ref, dims,
                        batch_size: int = DEFAULT_QUERY_BATCH) -> list:
     """service.py:97-125 -- all d*d fields for one reference point, row-major."""

@@ -158,3 +158,19 @@ def test_training_pair_draws_match_reference(refndf, monkeypatch):
     monkeypatch.setattr(ours, "targets", never)
     with pytest.raises(ndf.DataError):
         ours.sample_pairs_with_targets(field, Cfg, np.random.default_rng(1), 5)
+
+
+def test_psnr_matches_reference(refndf):
+    """service.compare_to_ground_truth's metric (training.py:162-180), restated."""
+    sys.path.insert(0, REF_SRC)
+    try:
+        from ndf import training as rtraining
+    finally:
+        sys.path.remove(REF_SRC)
+    rng = np.random.default_rng(2)
+    t = rng.normal(size=500)
+    for p in (t + 1e-3 * rng.normal(size=500), t.copy(), t + 1.0):
+        assert ndf.psnr(p, t) == rtraining.psnr(p, t)
+        assert ndf.psnr(p, t, peak=3.0) == rtraining.psnr(p, t, peak=3.0)
+    with pytest.raises(ndf.ParameterError):
+        ndf.psnr([], [])

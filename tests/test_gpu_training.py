@@ -62,3 +62,25 @@ def test_sample_pairs_with_targets_gpu():
     want = np.array([O.ksg_mi(x, y, 3) for x, y in zip(O.sample_many(grids, p_mu),
                                                        O.sample_many(grids, p_nu))])
     assert np.array_equal(t, want)
+
+
+def test_compare_to_ground_truth_vs_oracle():
+    """service.py:135-155 on the GPU: PSNR / max error / error field of the reconstruction
+    against the ground-truth field, vs the same quantities from the oracle."""
+    w = W.CONFIGS[0]
+    field = W.generate_host(w)
+    model = W.build_model(w, seed=0, grid_init=1.0)
+    om = O.OracleModel(model.spec.fourier_octaves, model.grid_mu, model.grid_nu, model.weights,
+                       model.biases, model.spec.merge, model.spec.activation, model.spec.head_kind)
+    ref = w.ref_position()
+    for role in (ndf.ROLE_MU, ndf.ROLE_NU):
+        res = ndf.compare_to_ground_truth(model, field, ndf.CorrelationMeasure("pearson"), ref,
+                                          w.dims, role)
+        recon = O.reconstruct_field(om, ref, w.dims, role=role)
+        truth = O.ground_truth_field(field.member_grids("v"), "pearson", ref, w.dims)
+        truth = np.where(np.isnan(truth), 0.0, truth).astype(np.float32)
+        err = recon.astype(np.float64) - truth.astype(np.float64)
+        assert abs(res.psnr_db - ndf.psnr(recon, truth)) <= 1e-3
+        assert abs(res.max_abs_err - np.max(np.abs(err))) <= 2e-5
+        assert res.error_field.dims == w.dims
+        assert np.max(np.abs(res.error_field.values - err.astype(np.float32))) <= 2e-5
