@@ -300,6 +300,35 @@ class NdfModel:
         for p in self.parameters():
             p.flags.writeable = False
 
+    def swapped_roles(self) -> "NdfModel":
+        """model.py:245-265 -- the (nu, mu) model sharing this model's parameters:
+        ``swapped.forward(p1, p2) == self.forward(p2, p1)`` (exact for the commutative
+        merges; concat reorders the first decoder layer's input blocks)."""
+        spec = replace(self.spec, var_mu=self.spec.var_nu, var_nu=self.spec.var_mu)
+        weights = list(self.weights)
+        if self.spec.merge == "concat" and not self.spec.shared:
+            half = self.spec.encoder_output_dim
+            w0 = weights[0]
+            weights[0] = np.concatenate([w0[half:], w0[:half]], axis=0)
+        if self.spec.shared:
+            return NdfModel(spec, self.grid_mu, self.grid_nu, weights, list(self.biases),
+                            self.enc_mu, self.enc_nu)
+        return NdfModel(spec, self.grid_nu, self.grid_mu, weights, list(self.biases),
+                        self.enc_nu, self.enc_mu)
+
+    def copy(self) -> "NdfModel":
+        """model.py:267-277 -- independent parameter arrays (device copies are rebuilt)."""
+        def cp(enc):
+            return ([w.copy() for w in enc[0]], [b.copy() for b in enc[1]])
+        grid_mu = self.grid_mu.copy()
+        enc_mu = cp(self.enc_mu)
+        if self.spec.shared:
+            grid_nu, enc_nu = grid_mu, enc_mu
+        else:
+            grid_nu, enc_nu = self.grid_nu.copy(), cp(self.enc_nu)
+        return NdfModel(self.spec, grid_mu, grid_nu, [w.copy() for w in self.weights],
+                        [b.copy() for b in self.biases], enc_mu, enc_nu)
+
     def with_precision(self, precision: str) -> "NdfModel":
         """Same parameters, other query precision (shares host arrays)."""
         return NdfModel(replace(self.spec, precision=precision), self.grid_mu, self.grid_nu,

@@ -174,3 +174,20 @@ def test_psnr_matches_reference(refndf):
         assert ndf.psnr(p, t, peak=3.0) == rtraining.psnr(p, t, peak=3.0)
     with pytest.raises(ndf.ParameterError):
         ndf.psnr([], [])
+
+
+def test_swapped_roles_and_copy_match_reference(refndf):
+    """NdfModel.swapped_roles / copy (model.py:245-277) on the conversion of reference
+    models: the same parameters as the reference's own swapped model, for a concat
+    (reordered first layer) and a shared spec."""
+    reference, rmodel = refndf
+    for kw in ({"merge": "concat", "encoder_layers": 2, "shared_encoder": False},
+               {"var_mu": "a", "var_nu": "b"}, {}):
+        spec = rmodel.ModelSpec(**kw) if kw else rmodel.ModelSpec()
+        theirs = rmodel.NdfModel.build(spec, seed=4)
+        ours = ndf.NdfModel.from_reference(theirs)
+        _same_params(ours.swapped_roles(), theirs.swapped_roles())
+        assert ours.swapped_roles().spec.var_mu == theirs.swapped_roles().spec.var_mu
+        c = ours.copy()
+        _same_params(c, theirs)
+        assert all(x is not y for x, y in zip(c.parameters(), ours.parameters()))

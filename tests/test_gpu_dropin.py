@@ -118,3 +118,23 @@ def test_embed_nodes_row_segments_vs_oracle():
             got = m.embed_nodes(branch, dims, v0, v1).cpu().numpy()
             want = O.embed(O.grid_positions_of(dims, np.arange(v0, v1)), table, 6)
             assert np.array_equal(got, want), (dims, branch)
+
+
+def test_swapped_roles_forward():
+    """model.py:245-265: swapped.forward(p1, p2) == forward(p2, p1) -- bitwise for the
+    commutative merges, to summation rounding for concat."""
+    from paper_2307_02203_b200.model import ModelSpec, NdfModel
+    rng = np.random.default_rng(8)
+    p1, p2 = rng.uniform(-1, 1, (256, 3)), rng.uniform(-1, 1, (256, 3))
+    for merge in ("sum_absdiff", "concat"):
+        # separate branches (var_mu != var_nu): a shared concat model has no swapped twin
+        # in the reference either (its decoder is not reordered, model.py:257)
+        spec = ModelSpec(measure_kind="pearson", grid_resolution=(5, 6, 3), precision="fp32",
+                         merge=merge, grid_init=1.0, var_mu="a", var_nu="b")
+        m = NdfModel.build(spec, seed=2)
+        got = m.swapped_roles().forward(p1, p2)
+        want = m.forward(p2, p1)
+        if merge == "concat":
+            assert np.max(np.abs(got - want)) <= 1e-6
+        else:
+            assert np.array_equal(got, want)
