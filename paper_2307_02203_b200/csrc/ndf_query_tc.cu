@@ -1765,10 +1765,21 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
     const size_t smem = (size_t)tc::make_x3_layout(a.m).smem_total;
     const bool silu = a.m.activation == NDF_ACT_SILU;
     // the value-range variant only when ndf_query_grid_stats asked for it
-    auto* kern = silu ? (a.stats ? tc::query_x3_kernel<true, true> : tc::query_x3_kernel<true, false>)
-                      : (a.stats ? tc::query_x3_kernel<false, true> : tc::query_x3_kernel<false, false>);
-    static SmemAttrCache attr[4];
-    if (e == cudaSuccess) e = attr[(silu ? 2 : 0) + (a.stats ? 1 : 0)].ensure(kern, smem);
+    static int f8 = -1;
+    if (f8 < 0) {
+      const char* ev = getenv("NDF_X3_F8");
+      f8 = ev ? atoi(ev) : 0;
+    }
+    using K = void (*)(const tc::TcArgs);
+    static const K kerns[8] = {
+        tc::query_x3_kernel<false, false, false>, tc::query_x3_kernel<false, true, false>,
+        tc::query_x3_kernel<true, false, false>,  tc::query_x3_kernel<true, true, false>,
+        tc::query_x3_kernel<false, false, true>,  tc::query_x3_kernel<false, true, true>,
+        tc::query_x3_kernel<true, false, true>,   tc::query_x3_kernel<true, true, true>};
+    const int ki = (f8 ? 4 : 0) + (silu ? 2 : 0) + (a.stats ? 1 : 0);
+    auto* kern = kerns[ki];
+    static SmemAttrCache attr[8];
+    if (e == cudaSuccess) e = attr[ki].ensure(kern, smem);
     if (e == cudaSuccess) e = launch_pdl(kern, g2, tc::kPPThreads, smem, s, t);
     count_launch();
     if (e != cudaSuccess) {
@@ -1894,7 +1905,7 @@ extern "C" void ndf_debug_tc_trace(long long* buf) { ndf::g_trace = buf; }
 static size_t tc_blob_total(const ndf_model_desc& m) {
   if (tc::x3_supported(m)) {
     const tc::X3Layout xl = tc::make_x3_layout(m);
-    return (size_t)xl.ext_off + (size_t)xl.ext_bytes;
+    return (size_t)xl.ext_off + (size_t)xl.ext_global;
   }
   return (size_t)tc::make_layout(m).blob_bytes;
 }

@@ -52,14 +52,25 @@ constexpr int kX3Slot = kX3Bx + kX3Byz + kX3ALat;
 constexpr int kX3Lat = 3 + 6 * kL;        // first latent feature (39)
 constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0) in bf16
 
+// NDF_X3_SHARED_EPI: all 16 epilogue warps serve the two slots in turn (see the epilogue)
+#ifndef NDF_X3_SHARED_EPI
+#define NDF_X3_SHARED_EPI 0
+#endif
+
 // Extension of the packed bf16 blob, after the standard layout (make_layout):
 //   wlat_hi, wlat_lo: N=128 x K=32 (k = 2c + {0: sum, 1: absdiff} of latent channel c),
 //                     canonical K-major, SBO 512 B
 //   wh_lo[l-1]:       lo parts of hidden layers 1..H-1, same layout as their hi parts
 //   wout32:           output weights, fp32
+//   (SMEM-resident part ends here: ext_bytes)
+//   wh_f8[l-1]:       fp8-corrected schedule (F8): per K32 step of hidden layer l, core
+//                     matrix 0 = E5M2(w) and core matrix 1 = E5M2(w - bf16(w)) for the
+//                     step's 16 K values; same bytes / layout as wh_lo, which it replaces
+//                     in SMEM
 struct X3Layout {
   int ext_off;
   int wlat_hi, wlat_lo, wh_lo, wout32, ext_bytes;
+  int wh_f8, ext_global;   // global-only region, total extension bytes
   int smem_w;      // resident weights: hidden W_hi + extension, 1024-aligned
   int smem_total;  // dynamic SMEM of query_x3_kernel
 };
@@ -73,8 +84,11 @@ __host__ __device__ inline X3Layout make_x3_layout(const ndf_model_desc& m) {
   x.wh_lo = 2 * 128 * 32 * 2;
   x.wout32 = x.wh_lo + (lay.H - 1) * lay.wh_bytes;
   x.ext_bytes = x.wout32 + kHid * 4;
+  x.wh_f8 = (x.ext_bytes + 1023) & ~1023;
+  x.ext_global = x.wh_f8 + (lay.H - 1) * lay.wh_bytes;
   x.smem_w = ((lay.H - 1) * lay.wh_bytes + x.ext_bytes + 1023) & ~1023;
-  x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2304;
+  x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2304 +
+                 (NDF_X3_SHARED_EPI ? 1024 : 0);   // shared epilogue: 3 dot partials per slot
   return x;
 }
 
@@ -310,6 +324,11 @@ __global__ void pack_x3_kernel(const ndf_model_desc m, uint8_t* blob) {
         const float w = hs * W[e];
         const float hi = __bfloat162float(__float2bfloat16_rn(w));
         *reinterpret_cast<__nv_bfloat16*>(dst + canon_off(nn, k, kSboA)) = __float2bfloat16_rn(w - hi);
+        // F8 pair: K32 step k >> 4, core matrix 0 = E5M2(w), 1 = E5M2(w - hi), 16 B per row
+        uint8_t* d8 = ext + xl.wh_f8 + (l - 1) * lay.wh_bytes +
+                      ((nn >> 3) * kSboA + (k >> 4) * 256 + (nn & 7) * 16 + (k & 15));
+        d8[0] = (uint8_t)(pack4_e5m2(w, 0.0f, 0.0f, 0.0f) & 0xffu);
+        d8[128] = (uint8_t)(pack4_e5m2(w - hi, 0.0f, 0.0f, 0.0f) & 0xffu);
       }
     } else {
       for (int64_t e = gtid; e < K; e += gsz)
@@ -350,7 +369,9 @@ __device__ __forceinline__ void latent_yx_direct(const float* __restrict__ lz, c
 
 // Hidden-layer epilogue of one 16-column sub-chunk, split operands: activation in fp32,
 // then 8 hi words into columns [0, 8) and 8 lo words into [8, 16) of the sub-chunk.
-template <bool SILU>
+// F8 (fp8-corrected schedule): columns [0, 8) = bf16(h) words, [8, 12) = E5M2(h - bf16(h)),
+// [12, 16) = E5M2(h) -- the K32 fp8 A operand of the correction MMA.
+template <bool SILU, bool F8>
 __device__ __forceinline__ void epilogue16_x3(const float* x, int act, uint32_t a_taddr) {
   float h[16];
   if constexpr (SILU) {
@@ -361,8 +382,23 @@ __device__ __forceinline__ void epilogue16_x3(const float* x, int act, uint32_t 
   }
   uint32_t p[16];
 #ifndef NDF_EXP_X3_NOSPLIT   // timing experiment: lo words zero (wrong results)
+  if constexpr (F8) {
+    float l[16];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) split_pair(h[2 * i], h[2 * i + 1], p[i], p[8 + i]);
+    for (int i = 0; i < 8; ++i) {
+      p[i] = pack2<false>(h[2 * i], h[2 * i + 1]);
+      ffma2(l[2 * i], l[2 * i + 1], __uint_as_float(p[i] << 16), __uint_as_float(p[i] & 0xffff0000u),
+            -1.0f, -1.0f, h[2 * i], h[2 * i + 1]);          // h - hi, exact
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      p[8 + i] = pack4_e5m2(l[4 * i], l[4 * i + 1], l[4 * i + 2], l[4 * i + 3]);
+      p[12 + i] = pack4_e5m2(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) split_pair(h[2 * i], h[2 * i + 1], p[i], p[8 + i]);
+  }
 #else
 #pragma unroll
   for (int i = 0; i < 8; ++i) { p[i] = pack2<false>(h[2 * i], h[2 * i + 1]); p[8 + i] = 0u; }
@@ -443,7 +479,8 @@ __host__ __device__ inline X3Tiles x3_tiles(int nx, int64_t v0, int64_t v1) {
 
 // RANGE: also reduce the outputs' min / max (ndf_query_grid_stats) -- a separate
 // instantiation: the three extra live registers cost the plain query 5% (measured)
-template <bool SILU, bool RANGE>
+// F8: fp8-corrected hidden layers (one bf16 MMA + one K32 E5M2 correction MMA per K16 step)
+template <bool SILU, bool RANGE, bool F8>
 __global__ void __launch_bounds__(kPPThreads, 1)
 query_x3_kernel(const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -543,8 +580,18 @@ query_x3_kernel(const TcArgs t) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(a.m.params_tc);
     for (int off = 0; off < whb; off += 32768)
       bulk_g2s(wh_s + off, src + lay.w0_bytes + off, (uint32_t)min(32768, whb - off), wbar);
-    for (int off = 0; off < xl.ext_bytes; off += 32768)
-      bulk_g2s(ext_s + off, src + xl.ext_off + off, (uint32_t)min(32768, xl.ext_bytes - off), wbar);
+    if constexpr (F8) {   // W_lat + (fp8 pairs in place of W_lo) + wout32
+      const int nlo = (H - 1) * lay.wh_bytes;
+      bulk_g2s(ext_s, src + xl.ext_off, (uint32_t)xl.wh_lo, wbar);
+      for (int off = 0; off < nlo; off += 32768)
+        bulk_g2s(ext_s + xl.wh_lo + off, src + xl.ext_off + xl.wh_f8 + off,
+                 (uint32_t)min(32768, nlo - off), wbar);
+      bulk_g2s(ext_s + xl.wout32, src + xl.ext_off + xl.wout32, (uint32_t)(xl.ext_bytes - xl.wout32),
+               wbar);
+    } else {
+      for (int off = 0; off < xl.ext_bytes; off += 32768)
+        bulk_g2s(ext_s + off, src + xl.ext_off + off, (uint32_t)min(32768, xl.ext_bytes - off), wbar);
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");   // prep tables ready
   if (tid < kC) eref_s[tid] = t.erefs[tid];
@@ -615,6 +662,11 @@ query_x3_kernel(const TcArgs t) {
               const uint64_t bh = smem_desc(whi + ks * 256, 128, kSboA);
               mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks), bh, idesc, 1u);
 #ifndef NDF_EXP_X3_ONEMMA    // timing experiment: hi x hi only (wrong results)
+              if constexpr (F8) {   // [E5M2(h_lo) | E5M2(h)] . [E5M2(w) ; E5M2(w_lo)], K32
+                mma_ts_f8_warp(d_next, a_tm + (uint32_t)(16 * ks + 8),
+                               smem_desc(wlo + ks * 256, 128, kSboA), idesc, 1u);
+                continue;
+              }
               mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks + 8), bh, idesc, 1u);
               if (use_lo) mma_ts_warp(d_next, a_tm + (uint32_t)(16 * ks),
                                       smem_desc(wlo + ks * 256, 128, kSboA), idesc, 1u);
@@ -707,6 +759,114 @@ query_x3_kernel(const TcArgs t) {
       }
     }
   } else {
+#if NDF_X3_SHARED_EPI
+    // ============ epilogue: all 16 warps serve slot 0 and slot 1 in turn =============
+    // Warp (j, wq): TMEM lane quarter wq, columns 64 it + 16 j (it = 0, 1) of every layer,
+    // so K-chunk k2 = columns [32 k2, 32 k2 + 32) is finished by warps j = 2 (k2 & 1) + {0, 1}
+    // at item k2 >> 1.  The slots' epilogues alternate (slot 0 layer l, slot 1 layer l,
+    // slot 0 layer l + 1, ...): each runs on the whole SM's MUFU while the other slot's
+    // layer MMAs run on the tensor pipe.
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
+    const int j = wg;                                 // 0..3
+    const bool lead = j == 0 && wq == 0;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    mbar_wait(wbar, 0);
+    const float bias_out = __ldg(reinterpret_cast<const float*>(
+        reinterpret_cast<const uint8_t*>(a.m.params_tc) + lay.vec_off) + H * kHid);
+    const uint32_t w32_addr = smem_u32(ext_s) + xl.wout32;
+    uint32_t acc_ph[kPPSlots] = {0u, 0u};
+    int64_t cnt_s[kPPSlots];
+#pragma unroll
+    for (int q = 0; q < kPPSlots; ++q) {
+      const int64_t f = (int64_t)blockIdx.x * kPPSlots + q;
+      cnt_s[q] = f < n_tiles ? (n_tiles - f + tile_stride - 1) / tile_stride : 0;
+    }
+    float z_pend[kPPSlots] = {0.0f, 0.0f};
+    int64_t kk_pend[kPPSlots] = {-1, -1};
+    RangeAcc rng;                                   // ndf_query_grid_stats only
+    auto flush = [&](int q) {
+      if (kk_pend[q] < 0) return;
+      int r, tx, ty;
+      decode((int64_t)blockIdx.x * kPPSlots + q + kk_pend[q] * tile_stride, r, tx, ty);
+      const int ix = kX3TX * tx + (wtid % kX3TX);
+      const int row = kX3TY * ty + (wtid / kX3TX);
+      const int64_t v = (int64_t)ix + (int64_t)a.nx * row;
+      if (ix < a.nx && row < nyz && v >= a.v0 && v < a.v1) {
+        const float o = head_exact(a.m.head, z_pend[q]);
+        if (t.out16) {
+          const __half ho = __float2half_rn(o);
+          t.out16[(int64_t)r * t.ld_out + (v - a.v0)] = *reinterpret_cast<const uint16_t*>(&ho);
+        } else {
+          a.out[v - a.v0] = o;
+          if constexpr (RANGE) rng.add(o);
+        }
+      }
+      kk_pend[q] = -1;
+    };
+#pragma unroll 1
+    for (int64_t kk = 0; kk < cnt_s[0]; ++kk) {
+#pragma unroll 1
+      for (int l = 0; l < H; ++l) {
+#pragma unroll
+        for (int q = 0; q < kPPSlots; ++q) {
+          if (kk >= cnt_s[q]) continue;
+          const uint32_t half = (uint32_t)((kk * H + l) & 1);
+          const uint32_t d_base = tmem_base + (uint32_t)(q * 2 * kHid) + lane_base + half * kHid;
+          mbar_wait(&acc_full[q], acc_ph[q]);
+          acc_ph[q] ^= 1u;
+          tc_fence_after();
+          if (l == 0 && lead && lane == 0) mbar_arrive(&s_free[q]);   // slot SMEM reusable
+          if (lead && lane == 0) NDF_X3_TRACE(q, (int)kk, 5 + 2 * l);
+          float va[16], vb[16];
+          tmem_ld16_nowait(d_base + 16u * (uint32_t)j, va);
+          tmem_ld16_nowait(d_base + 64u + 16u * (uint32_t)j, vb);
+          tmem_wait_ld();
+          if (l + 1 < H) {
+            epilogue16_x3<SILU, F8>(va, a.m.activation, d_base + 16u * (uint32_t)j);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            named_bar_arrive(1 + 4 * q + (j >> 1), 288);
+            epilogue16_x3<SILU, F8>(vb, a.m.activation, d_base + 64u + 16u * (uint32_t)j);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            named_bar_arrive(1 + 4 * q + 2 + (j >> 1), 288);
+            if (lead && lane == 0) NDF_X3_TRACE(q, (int)kk, 6 + 2 * l);
+            if (l == 0 && j == 0) flush(q);
+          } else {
+            if (lead && lane == 0) mbar_arrive(&d_free[q]);
+            float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            dot16_x3<SILU>(va, 16 * j, a.m.activation, w32_addr, dots);
+            dot16_x3<SILU>(vb, 64 + 16 * j, a.m.activation, w32_addr, dots);
+            tc_fence_before();
+            const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
+            float* dx = dotx + q * 3 * kTileM;
+            if (j > 0) {
+              dx[(j - 1) * kTileM + wtid] = part;
+              named_bar_arrive(9 + q, 512);
+            } else {
+              named_bar(9 + q, 512);
+              z_pend[q] = ((part + dx[wtid]) + (dx[kTileM + wtid] + dx[2 * kTileM + wtid])) + bias_out;
+              kk_pend[q] = kk;
+              if (H == 1) flush(q);
+            }
+            if (lead && lane == 0) NDF_X3_TRACE(q, (int)kk, 6 + 2 * l);
+          }
+        }
+      }
+    }
+    if (j == 0) {
+      flush(0);
+      flush(1);
+    }
+    if constexpr (RANGE) {
+      if (j == 0) rng.flush(a.stats);
+    }
+    (void)rng;
+    (void)n;
+    (void)cnt;
+    (void)first;
+    (void)d_slot;
+#else
     // ======================== epilogue (slot s, column half ch) ======================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
     const int ch = wg & 1;
@@ -774,7 +934,7 @@ query_x3_kernel(const TcArgs t) {
             float* cur = (i & 1) ? vb : va;
             float* nxt = (i & 1) ? va : vb;
             if (i + 1 < 4) tmem_ld16_nowait(d_base + col + 32u, nxt);
-            epilogue16_x3<SILU>(cur, a.m.activation, d_base + col);
+            epilogue16_x3<SILU, F8>(cur, a.m.activation, d_base + col);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             named_bar_arrive(1 + 4 * s + i, 288);
@@ -826,6 +986,7 @@ query_x3_kernel(const TcArgs t) {
     }
     (void)rng;
     (void)n;
+#endif
   }
   tc_fence_before();
   __syncthreads();

@@ -119,6 +119,29 @@ __device__ __forceinline__ void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, ui
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// fp8 x fp8 -> fp32 (kind::f8f6f4; with a_format = b_format = 1 = E5M2 the instruction
+// descriptor has the same bits as the bf16 one): one K32 step, A from TMEM (4 elements per
+// 32-bit column, k ascending from the low byte)
+__device__ __forceinline__ void mma_ts_f8_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// four fp32 values -> four E5M2 bytes (round to nearest even, saturating), v0 in the low byte
+__device__ __forceinline__ uint32_t pack4_e5m2(float v0, float v1, float v2, float v3) {
+  uint32_t w;
+  asm("{\n\t.reg .b16 l, h;\n\t"
+      "cvt.rn.satfinite.e5m2x2.f32 l, %2, %1;\n\t"
+      "cvt.rn.satfinite.e5m2x2.f32 h, %4, %3;\n\t"
+      "mov.b32 %0, {l, h};\n}"
+      : "=r"(w)
+      : "f"(v0), "f"(v1), "f"(v2), "f"(v3));
+  return w;
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

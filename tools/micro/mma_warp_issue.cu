@@ -94,6 +94,14 @@ __global__ void k(long long* out, int n_mma, int ts, int N, int issuers, int cha
                       smem_desc(b + bo + kk * 256, 128, 2048), idesc, 1u);
         }
       }
+    } else if (chains >= 100) {   // two accumulators in bursts of (chains - 100) MMAs
+      const int burst = chains - 100;
+#pragma unroll 1
+      for (int i = 0; i < n_mma; ++i) {
+        const int kk = i & 7, c = (i / burst) & 1;
+        mma_ts_warp(tm + dcol + (uint32_t)(c * N), tm + acol + 16 * kk,
+                    smem_desc(b + kk * 256, 128, 2048), idesc, 1u);
+      }
     } else {   // four accumulators N apart
       const uint32_t bo = (uint32_t)(N * 256);
 #pragma unroll 1
@@ -129,13 +137,11 @@ int main() {
   // issuers: bitmask of warps (warp w runs on SMSP w % 4); chains 2: alternating accumulators
   struct C { int ts, N, mask, ch; const char* name; } cfgs[] = {
       {1, 128, 0x1, 1, "TS N128 1 chain                      "},
-      {1, 64, 0x1, 1, "TS N64 1 chain                       "},
-      {1, 32, 0x1, 1, "TS N32 1 chain                       "},
-      {1, 128, 0x1, 2, "TS N128 2 chains (cols 0 / 128)      "},
-      {1, 64, 0x1, 2, "TS N64 2 chains (column halves)      "},
-      {1, 32, 0x1, 4, "TS N32 4 chains (column quarters)    "},
-      {0, 64, 0x1, 2, "SS N64 2 chains (column halves)      "},
-      {0, 128, 0x1, 2, "SS N128 2 chains                     "}};
+      {1, 128, 0x1, 2, "TS N128 2 accumulators, alternating  "},
+      {1, 128, 0x1, 102, "TS N128 2 accumulators, bursts of 2  "},
+      {1, 128, 0x1, 103, "TS N128 2 accumulators, bursts of 3  "},
+      {1, 128, 0x1, 106, "TS N128 2 accumulators, bursts of 6  "},
+      {1, 128, 0x1, 125, "TS N128 2 accumulators, bursts of 25 "}};
   for (auto c : cfgs) {
     k<<<148, 256, 98304>>>(d, n, c.ts, c.N, c.mask, c.ch);
     long long h[8 * 148];
