@@ -84,3 +84,30 @@ def test_compare_to_ground_truth_vs_oracle():
         assert abs(res.max_abs_err - np.max(np.abs(err))) <= 2e-5
         assert res.error_field.dims == w.dims
         assert np.max(np.abs(res.error_field.values - err.astype(np.float32))) <= 2e-5
+
+
+def test_targets_two_variables_and_ksg_compare():
+    """Targets across two variables (var_mu != var_nu, training.py:114-115) and the KSG
+    ground truth in compare_to_ground_truth."""
+    w = W.CONFIGS[0]
+    f = W.generate_host(w)
+    v = f.member_grids("v")
+    u = np.ascontiguousarray(np.tanh(v) + 0.1 * v * v, dtype=np.float32)   # a second variable
+    field = ndf.EnsembleField(f.domain, ("v", "u"), np.stack([v, u]))
+    rng = np.random.default_rng(9)
+    p_mu, p_nu = rng.uniform(-1, 1, (200, 3)), rng.uniform(-1, 1, (200, 3))
+    for meas in (ndf.CorrelationMeasure("pearson"), ndf.CorrelationMeasure("ksg_mi", ksg_k=4)):
+        got = ndf.targets(field, meas, "v", "u", p_mu, p_nu)
+        a, b = O.sample_many(v, p_mu), O.sample_many(u, p_nu)
+        if meas.kind == "pearson":
+            assert np.max(np.abs(got - O.pearson_rowwise(a, b))) <= 1e-12
+        else:
+            assert np.array_equal(got, [O.ksg_mi(a[i], b[i], 4) for i in range(len(a))])
+    model = W.build_model(w, seed=0, grid_init=1.0)
+    res = ndf.compare_to_ground_truth(model, f, ndf.CorrelationMeasure("ksg_mi", ksg_k=3),
+                                      w.ref_position(), w.dims)
+    truth = O.ground_truth_field(v, "ksg_mi", w.ref_position(), w.dims, k=3)
+    om = O.OracleModel(model.spec.fourier_octaves, model.grid_mu, model.grid_nu, model.weights,
+                       model.biases, model.spec.merge, model.spec.activation, model.spec.head_kind)
+    recon = O.reconstruct_field(om, w.ref_position(), w.dims)
+    assert abs(res.psnr_db - ndf.psnr(recon, truth.astype(np.float32))) <= 1e-3
