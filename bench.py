@@ -760,6 +760,37 @@ def secondary(args, line, rank, world, dev, peaks, peak_kind, model, w):
     if rank == 0:
         line["c4_bulk_pairs"] = c4l
     ens2.drop_derived()
+    # ---- F2's caller: training targets (training.py:111-119) of uniform off-grid pairs --
+    if rank == 0:
+        tp = 1 << 16
+        trng = np.random.default_rng(12)
+        tmu, tnu = trng.uniform(-1.0, 1.0, (tp, 3)), trng.uniform(-1.0, 1.0, (tp, 3))
+        tm = ndf.CorrelationMeasure("ksg_mi", ksg_k=W.CONFIGS[4].ksg_k)
+        tpe = ndf.CorrelationMeasure("pearson")
+        ndf.targets_device(ens2, tpe, "v", "v", tmu, tnu)   # warm-up: builds the vertex-major copy
+        t_ms = ev_ms(lambda: ndf.targets_device(ens2, tm, "v", "v", tmu, tnu), 1, 0, flushing=False)
+        tp_ms = ev_ms(lambda: ndf.targets_device(ens2, tpe, "v", "v", tmu, tnu), 3, 1, flushing=False)
+        tl = {"pairs": tp, "ksg_ms": t_ms, "pearson_ms": tp_ms, "pairs_per_s": tp / (t_ms * 1e-3),
+              "k": W.CONFIGS[4].ksg_k,
+              "note": "public targets_device over uniform off-grid position pairs of the config-2 "
+                      "ensemble: fp64 trilinear samples from the variable's vertex-major copy (built "
+                      "once per variable, in the warm-up) into HBM, one KSG (or Pearson) launch"}
+        if cpu:
+            nc = min(args.cpu_c4_pairs, tp)
+            # the samples the reference's sample_many would produce (bit-identical, tests)
+            A = ens2.sample_many(tmu[:nc]).cpu().numpy()
+            B = ens2.sample_many(tnu[:nc]).cpu().numpy()
+            parts = [(A[i::procs * 2], B[i::procs * 2], W.CONFIGS[4].ksg_k) for i in range(procs * 2)]
+            tc = time.perf_counter()
+            with ProcessPoolExecutor(max_workers=procs) as ex:
+                list(ex.map(_c4_cpu_chunk, parts))
+            cdt = time.perf_counter() - tc
+            tl["cpu_baseline"] = {"value": nc / cdt, "unit": "pairs/s", "cores": procs, "kind": "port",
+                                  "sample": f"{nc} of the pairs: oracle pearson_rowwise + ksg_mi per "
+                                            f"pair (scipy cKDTree) in {procs} processes on their "
+                                            f"samples ({cdt:.1f} s wall; sampling untimed)"}
+            tl["speedup_vs_cpu"] = tl["pairs_per_s"] / tl["cpu_baseline"]["value"]
+        line["training_targets"] = tl
     del ens2
     torch.cuda.empty_cache()
     # ---- config 3: 64-reference cube, both heads, the benched precision ---------------

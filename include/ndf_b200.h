@@ -169,6 +169,14 @@ int ndf_sample_many_ld(const float* X, int32_t M, int64_t ld, int64_t col0, int3
                        int32_t ny, int32_t nz, const double* pos, int64_t B, double* out,
                        void* stream);
 
+/* sample_many from the vertex-major copy Xv (V, M) of one variable (ndf_vertex_major):
+ * the same fp64 trilinear samples bit for bit, but each lattice corner's M members are one
+ * contiguous row, so a batch of scattered positions reads whole rows instead of one 32-byte
+ * sector per member and corner -- the layout for large batches (training targets,
+ * training.py:111-119). */
+int ndf_sample_many_vm(const float* Xv, int32_t M, int32_t nx, int32_t ny, int32_t nz,
+                       const double* pos, int64_t B, double* out, void* stream);
+
 /* Ground-truth Pearson field in ONE streaming read of X: out[v - v0] = pearson of node
  * column v against ref_vec (fp64, M; device) for v in [v0, v1) -- measures.py:84-108 over
  * a node-aligned ground_truth_field (measures.py:286-295): fp64 shifted moments per

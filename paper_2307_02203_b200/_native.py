@@ -83,6 +83,7 @@ SIGNATURES = {
     "ndf_query_grid_multi": (ctypes.c_int, [ctypes.POINTER(ModelDesc), _c_p, _i32, _i32, _i32,
                                             _i32, _i32, _i64, _i64, _c_p, _i64, _c_p]),
     "ndf_sample_many": (ctypes.c_int, [_c_p, _i32, _i32, _i32, _i32, _c_p, _i64, _c_p, _c_p]),
+    "ndf_sample_many_vm": (ctypes.c_int, [_c_p, _i32, _i32, _i32, _i32, _c_p, _i64, _c_p, _c_p]),
     "ndf_sample_many_ld": (ctypes.c_int, [_c_p, _i32, _i64, _i64, _i32, _i32, _i32, _c_p, _i64,
                                           _c_p, _c_p]),
     "ndf_pearson_field": (ctypes.c_int, [_c_p, _i32, _i64, _i64, _c_p, _i64, _i64, _c_p, _c_p]),

@@ -73,6 +73,39 @@ __global__ void sample_many_kernel(const float* __restrict__ X, int M, int64_t l
   out[idx] = acc;
 }
 
+// Same samples from the vertex-major copy Xv (V, M): consecutive threads are consecutive
+// members of one position, so each corner read is a contiguous row segment.
+__global__ void sample_many_vm_kernel(const float* __restrict__ Xv, int M, int nx, int ny, int nz,
+                                      const double* __restrict__ pos, int64_t B,
+                                      double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * (int64_t)M) return;
+  const int64_t b = idx / M;
+  const int m = (int)(idx - b * M);
+  int ix, iy, iz;
+  double tx, ty, tz;
+  frac_index(pos[3 * b + 0], nx, ix, tx);
+  frac_index(pos[3 * b + 1], ny, iy, ty);
+  frac_index(pos[3 * b + 2], nz, iz, tz);
+  double acc = 0.0;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    const double wz = dz ? tz : dsub(1.0, tz);
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const double wy = dy ? ty : dsub(1.0, ty);
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const double wx = dx ? tx : dsub(1.0, tx);
+        const double w = dmul(dmul(wz, wy), wx);
+        const int64_t vtx = (int64_t)(iz + dz) * ny * nx + (int64_t)(iy + dy) * nx + (ix + dx);
+        acc = dadd(acc, dmul(w, (double)__ldg(Xv + vtx * M + m)));
+      }
+    }
+  }
+  out[idx] = acc;
+}
+
 // ---- fused Pearson field: one streaming read of X ---------------------------
 // r[v] = sum_m (x_mv - mu_v)(ref_m - mu_r) / sqrt(var_v * var_r), measures.py:84-108,
 // computed per vertex in ONE pass over its member column: shifted fp64 moments
@@ -632,6 +665,21 @@ extern "C" int ndf_sample_many_ld(const float* X, int32_t M, int64_t ld, int64_t
   const int threads = 256;
   sample_many_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
       X, M, ld, col0, nx, ny, nz, pos, B, out);
+  NDF_LAUNCH_CHECK();
+  return NDF_OK;
+}
+
+extern "C" int ndf_sample_many_vm(const float* Xv, int32_t M, int32_t nx, int32_t ny, int32_t nz,
+                                  const double* pos, int64_t B, double* out, void* stream) {
+  NDF_REQUIRE(M >= 1 && nx >= 2 && ny >= 2 && nz >= 2, NDF_ERR_PARAMETER,
+              "sample_many: need M >= 1 and >= 2 nodes per axis");
+  NDF_REQUIRE(B >= 0, NDF_ERR_PARAMETER, "negative batch");
+  if (B == 0) return NDF_OK;
+  NDF_REQUIRE(Xv && pos && out, NDF_ERR_PARAMETER, "null pointer");
+  const int64_t n = B * (int64_t)M;
+  const int threads = 256;
+  sample_many_vm_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+      Xv, M, nx, ny, nz, pos, B, out);
   NDF_LAUNCH_CHECK();
   return NDF_OK;
 }

@@ -211,8 +211,12 @@ class DeviceEnsemble:
         B = int(pos.shape[0])
         out = torch.empty((B, self.member_count), dtype=torch.float64, device=self.device)
         d = self.domain
-        N.call("ndf_sample_many_ld", N.ptr(self.X), self.member_count, self.ld, self.col0, d.nx,
-               d.ny, d.nz, N.ptr(pos), B, N.ptr(out), N.stream_handle(self.device))
+        if self._xv is not None:         # vertex-major copy built: whole-row corner reads
+            N.call("ndf_sample_many_vm", N.ptr(self._xv), self.member_count, d.nx, d.ny, d.nz,
+                   N.ptr(pos), B, N.ptr(out), N.stream_handle(self.device))
+        else:
+            N.call("ndf_sample_many_ld", N.ptr(self.X), self.member_count, self.ld, self.col0,
+                   d.nx, d.ny, d.nz, N.ptr(pos), B, N.ptr(out), N.stream_handle(self.device))
         return out
 
 

@@ -5,7 +5,8 @@
 The reference samples both position sets with ``sample_many`` (fp64 trilinear over all
 M members, ensemble.py:130-167) and then runs ``pearson_rowwise`` (measures.py:111-133)
 or a Python loop of ``ksg_mi`` (measures.py:173-203), one pair at a time.  Here the
-samples stay in HBM (``ndf_sample_many_ld`` writes the (B, M) fp64 rows) and ONE
+samples stay in HBM (``ndf_sample_many_vm`` writes the (B, M) fp64 rows from the variable's
+vertex-major copy, built once for large batches; ``ndf_sample_many_ld`` otherwise) and ONE
 ``ndf_pearson_rows`` or ``ndf_ksg_rows`` launch per chunk evaluates every pair: Pearson
 within 1e-12 of the reference (NaN for a constant row, exactly 1.0 for identical rows,
 as ``pearson_rowwise``), KSG MI bit-identical.  ``sample_pairs_with_targets`` keeps the
@@ -51,6 +52,11 @@ def targets_device(field_obj, measure: CorrelationMeasure, var_mu: str, var_nu: 
     if B == 0:
         return out
     stream = N.stream_handle(dev)
+    # large batches: sample from a vertex-major copy (built once per variable, kept by the
+    # DeviceEnsemble) -- every lattice corner's members are one contiguous row there
+    for d_ in (dmu, dnu):
+        if B * M >= d_.node_count and d_.col0 == 0 and d_.ld == d_.node_count:
+            d_.vertex_major()
     if measure.kind == "ksg_mi":
         k = measure.ksg_k
         if not 1 <= k <= M - 1:

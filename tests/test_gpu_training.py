@@ -111,3 +111,22 @@ def test_targets_two_variables_and_ksg_compare():
                        model.biases, model.spec.merge, model.spec.activation, model.spec.head_kind)
     recon = O.reconstruct_field(om, w.ref_position(), w.dims)
     assert abs(res.psnr_db - ndf.psnr(recon, truth.astype(np.float32))) <= 1e-3
+
+
+def test_sample_many_vertex_major_bitwise():
+    """ndf_sample_many_vm (vertex-major source) == ndf_sample_many_ld, bit for bit, and the
+    oracle's sample_many (ensemble.py:130-167)."""
+    w = W.CONFIGS[0]
+    field = W.generate_host(w)
+    from paper_2307_02203_b200.ensemble import _device_view
+    d = _device_view(field, "v")
+    rng = np.random.default_rng(13)
+    pos = np.concatenate([rng.uniform(-1.2, 1.2, (777, 3)), O.grid_positions(w.dims)[:50],
+                          [[1.0, 1.0, 1.0], [-1.0, -1.0, -1.0]]])
+    d.drop_derived()
+    mm = d.sample_many(pos).cpu().numpy()
+    d.vertex_major()
+    vm = d.sample_many(pos).cpu().numpy()
+    d.drop_derived()
+    assert np.array_equal(mm, vm)
+    assert np.array_equal(vm, O.sample_many(field.member_grids("v"), pos))
