@@ -298,6 +298,7 @@ def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: st
                    N.ptr(out), stream)
         else:
             pos = grid_positions(dims)[v0:v1]
+            _vertex_major_for(dnu, len(pos))
             buf = torch.empty(min(chunk, max(len(pos), 1)), dtype=torch.float64, device=dev)
             for s in range(0, len(pos), chunk):
                 rows = dnu.sample_many(pos[s:s + chunk])
@@ -318,6 +319,7 @@ def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: st
                    N.ptr(status), stream)
         else:
             pos = grid_positions(dims)[v0:v1]
+            _vertex_major_for(dnu, len(pos))
             for s in range(0, len(pos), chunk):
                 rows = dnu.sample_many(pos[s:s + chunk])
                 n = rows.shape[0]
@@ -326,6 +328,14 @@ def ground_truth_field_device(field_obj, measure: CorrelationMeasure, var_mu: st
         if int(status.item()):
             raise ParameterError("digamma defined here for positive arguments only")
     return out
+
+
+def _vertex_major_for(d, n_positions: int) -> None:
+    """Off-node sampling of many positions reads whole member rows from the variable's
+    vertex-major copy (ndf_sample_many_vm, bit-identical): build it once when the sampling
+    would touch at least as many values as the copy costs to write."""
+    if n_positions * d.member_count >= d.node_count and d.col0 == 0 and d.ld == d.node_count:
+        d.vertex_major()
 
 
 def ground_truth_field(field_obj, measure: CorrelationMeasure, var_mu: str, var_nu: str, ref,
