@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define NDF_ABI_VERSION 2
+#define NDF_ABI_VERSION 3
 #define NDF_MAX_LAYERS 8
 #define NDF_MAX_WIDTH 256
 #define NDF_MAX_LEVELS 16

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("NDF_LIB_PATH") or os.path.join(HERE, "libndf_b200.so"
 NDF_MAX_LAYERS = 8
 NDF_MAX_WIDTH = 256
 NDF_MAX_LEVELS = 16
-NDF_ABI_VERSION = 2
+NDF_ABI_VERSION = 3
 
 MERGE = {"multiply": 0, "concat": 1, "add": 2, "absdiff": 3, "sum_absdiff": 4}
 ACT = {"relu": 0, "snake": 1, "snake_alt": 2, "silu": 3}

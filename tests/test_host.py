@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES), set(syms) ^ set(N.SIGNATURES)
-    assert lib.ndf_abi_version() == N.NDF_ABI_VERSION == 2
+    assert lib.ndf_abi_version() == N.NDF_ABI_VERSION == 3
 
 
 def test_status_mapping():
