@@ -54,7 +54,7 @@ constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0) in bf16
 
 // NDF_X3_SHARED_EPI: all 16 epilogue warps serve the two slots in turn (see the epilogue)
 #ifndef NDF_X3_SHARED_EPI
-#define NDF_X3_SHARED_EPI 0
+#define NDF_X3_SHARED_EPI 1
 #endif
 
 // Extension of the packed bf16 blob, after the standard layout (make_layout):
