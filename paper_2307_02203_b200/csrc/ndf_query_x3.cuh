@@ -52,6 +52,12 @@ constexpr int kX3Slot = kX3Bx + kX3Byz + kX3ALat;
 constexpr int kX3Lat = 3 + 6 * kL;        // first latent feature (39)
 constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0) in bf16
 
+// NDF_X3_EARLY_BIAS: the issuer initialises each hidden layer's accumulator with its bias as
+// soon as the previous layer's MMAs are done, instead of with the first K-chunk
+#ifndef NDF_X3_EARLY_BIAS
+#define NDF_X3_EARLY_BIAS 1
+#endif
+
 // NDF_X3_SHARED_EPI: all 16 epilogue warps serve the two slots in turn (see the epilogue)
 #ifndef NDF_X3_SHARED_EPI
 #define NDF_X3_SHARED_EPI 1
@@ -502,6 +508,7 @@ query_x3_kernel(const TcArgs t) {
   uint64_t* d_free = &bars[5];
   uint64_t* b_full = &bars[7];                    // [kPPSlots] the tile's PX / PYZ rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* e2_done = &bars[24];                  // [slot] last-layer TMEM reads of a tile done
   float* eref_s = reinterpret_cast<float*>(bars + 16);
   float* dotx = reinterpret_cast<float*>(bars + 32);     // [2 tile parities][kPPSlots][128]
 
@@ -530,6 +537,7 @@ query_x3_kernel(const TcArgs t) {
       mbar_init(&s_free[s], 1);
       mbar_init(&d_free[s], 1);
       mbar_init(&b_full[s], 1);
+      mbar_init(&e2_done[s], NDF_X3_SHARED_EPI ? 16 : 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -639,6 +647,19 @@ query_x3_kernel(const TcArgs t) {
           const bool use_lo = (wlo_mask >> (l + 1)) & 1u;
           // x3_burst: 0 = issue K-chunk by K-chunk as the epilogue completes them,
           // 1 = the whole layer after the epilogue, 2 = pairs of K-chunks
+#if NDF_X3_EARLY_BIAS
+          // layer l's MMAs are done (they read A_l from the half layer l + 1 accumulates
+          // into): initialise that half with the bias now, ahead of the epilogue's K-chunks
+          mbar_wait(&acc_full[si], (uint32_t)((kk * H + l) & 1));
+          // l == 0: the target half held the previous tile's last layer -- wait until its
+          // epilogue has read it
+          if (l == 0 && kk > 0) mbar_wait(&e2_done[si], (uint32_t)((kk - 1) & 1));
+          tc_fence_after();
+          mma_ss_warp(d_next, smem_desc(smem_u32(bias_s), (uint32_t)(H * kX3Blk), 128),
+                      smem_desc(smem_u32(bias_s) + (uint32_t)((l + 1) * kX3Blk),
+                                (uint32_t)((H - l - 1) * kX3Blk), 128),
+                      idesc, 0u);
+#endif
           if (t.x3_burst == 1)
             for (int k2 = 0; k2 < 4; ++k2) named_bar(1 + 4 * si + k2, 288);
 #pragma unroll 1
@@ -651,7 +672,7 @@ query_x3_kernel(const TcArgs t) {
             // the whole issuer warp runs this (elect.sync inside the MMA asm): operands
             // stay in uniform registers, MMAs go out back to back
             tc_fence_after();
-            if (k2 == 0)
+            if (k2 == 0 && !NDF_X3_EARLY_BIAS)
               mma_ss_warp(d_next, smem_desc(smem_u32(bias_s), (uint32_t)(H * kX3Blk), 128),
                           smem_desc(smem_u32(bias_s) + (uint32_t)((l + 1) * kX3Blk),
                                     (uint32_t)((H - l - 1) * kX3Blk), 128),
@@ -834,6 +855,8 @@ query_x3_kernel(const TcArgs t) {
             if (l == 0 && j == 0) flush(q);
           } else {
             if (lead && lane == 0) mbar_arrive(&d_free[q]);
+            tc_fence_before();
+            if (lane == 0) mbar_arrive(&e2_done[q]);       // this warp's TMEM reads are done
             float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             dot16_x3<SILU>(va, 16 * j, a.m.activation, w32_addr, dots);
             dot16_x3<SILU>(vb, 64 + 16 * j, a.m.activation, w32_addr, dots);
@@ -960,6 +983,7 @@ query_x3_kernel(const TcArgs t) {
             if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
           }
           tc_fence_before();
+          if (lane == 0) mbar_arrive(&e2_done[s]);          // this warp's TMEM reads are done
           const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
           float* dx = dotx + ((kk & 1) * kPPSlots + s) * kTileM;
           if (wq == 0 && lane == 0) NDF_X3_TRACE(s, (int)kk, 20 + ch);
