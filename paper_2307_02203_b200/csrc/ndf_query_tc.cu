@@ -1765,20 +1765,24 @@ static int run_x3(tc::TcArgs t, const double* refs_dev, int n_ref, cudaStream_t 
     const size_t smem = (size_t)tc::make_x3_layout(a.m).smem_total;
     const bool silu = a.m.activation == NDF_ACT_SILU;
     // the value-range variant only when ndf_query_grid_stats asked for it
-    static int f8 = -1;
+    static int f8 = -1, shared_env = -2;
     if (f8 < 0) {
       const char* ev = getenv("NDF_X3_F8");
       f8 = ev ? atoi(ev) : 0;
+      const char* es = getenv("NDF_X3_SHARED");
+      shared_env = es ? atoi(es) : -1;
     }
+    const bool shared = shared_env >= 0 ? shared_env != 0 : n_ref == 1;
     using K = void (*)(const tc::TcArgs);
-    static const K kerns[8] = {
-        tc::query_x3_kernel<false, false, false>, tc::query_x3_kernel<false, true, false>,
-        tc::query_x3_kernel<true, false, false>,  tc::query_x3_kernel<true, true, false>,
-        tc::query_x3_kernel<false, false, true>,  tc::query_x3_kernel<false, true, true>,
-        tc::query_x3_kernel<true, false, true>,   tc::query_x3_kernel<true, true, true>};
-    const int ki = (f8 ? 4 : 0) + (silu ? 2 : 0) + (a.stats ? 1 : 0);
+#define NDF_X3_K(SH, F)                                                                         \
+  tc::query_x3_kernel<false, false, F, SH>, tc::query_x3_kernel<false, true, F, SH>,           \
+      tc::query_x3_kernel<true, false, F, SH>, tc::query_x3_kernel<true, true, F, SH>
+    static const K kerns[16] = {NDF_X3_K(false, false), NDF_X3_K(false, true),
+                                NDF_X3_K(true, false), NDF_X3_K(true, true)};
+#undef NDF_X3_K
+    const int ki = (shared ? 8 : 0) + (f8 ? 4 : 0) + (silu ? 2 : 0) + (a.stats ? 1 : 0);
     auto* kern = kerns[ki];
-    static SmemAttrCache attr[8];
+    static SmemAttrCache attr[16];
     if (e == cudaSuccess) e = attr[ki].ensure(kern, smem);
     if (e == cudaSuccess) e = launch_pdl(kern, g2, tc::kPPThreads, smem, s, t);
     count_launch();

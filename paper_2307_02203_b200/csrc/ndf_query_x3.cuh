@@ -58,10 +58,9 @@ constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0) in bf16
 #define NDF_X3_EARLY_BIAS 1
 #endif
 
-// NDF_X3_SHARED_EPI: all 16 epilogue warps serve the two slots in turn (see the epilogue)
-#ifndef NDF_X3_SHARED_EPI
-#define NDF_X3_SHARED_EPI 1
-#endif
+// SHARED (template): all 16 epilogue warps serve the two slots in turn (see the epilogue); the
+// launcher takes it for single-reference queries (c1: 0.2994 vs 0.3022 ms) and the per-slot
+// warps for multi-reference cubes (c3: 41.0 vs 43.2 ms); NDF_X3_SHARED=0/1 overrides
 
 // Extension of the packed bf16 blob, after the standard layout (make_layout):
 //   wlat_hi, wlat_lo: N=128 x K=32 (k = 2c + {0: sum, 1: absdiff} of latent channel c),
@@ -94,7 +93,7 @@ __host__ __device__ inline X3Layout make_x3_layout(const ndf_model_desc& m) {
   x.ext_global = x.wh_f8 + (lay.H - 1) * lay.wh_bytes;
   x.smem_w = ((lay.H - 1) * lay.wh_bytes + x.ext_bytes + 1023) & ~1023;
   x.smem_total = x.smem_w + (lay.H + 1) * kX3Blk + kX3SelX + kX3SelYZ + kPPSlots * kX3Slot + 2304 +
-                 (NDF_X3_SHARED_EPI ? 1024 : 0);   // shared epilogue: 3 dot partials per slot
+                 1024;   // + the shared epilogue's 3 dot partials per slot
   return x;
 }
 
@@ -486,7 +485,7 @@ __host__ __device__ inline X3Tiles x3_tiles(int nx, int64_t v0, int64_t v1) {
 // RANGE: also reduce the outputs' min / max (ndf_query_grid_stats) -- a separate
 // instantiation: the three extra live registers cost the plain query 5% (measured)
 // F8: fp8-corrected hidden layers (one bf16 MMA + one K32 E5M2 correction MMA per K16 step)
-template <bool SILU, bool RANGE, bool F8>
+template <bool SILU, bool RANGE, bool F8, bool SHARED>
 __global__ void __launch_bounds__(kPPThreads, 1)
 query_x3_kernel(const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -537,7 +536,7 @@ query_x3_kernel(const TcArgs t) {
       mbar_init(&s_free[s], 1);
       mbar_init(&d_free[s], 1);
       mbar_init(&b_full[s], 1);
-      mbar_init(&e2_done[s], NDF_X3_SHARED_EPI ? 16 : 8);
+      mbar_init(&e2_done[s], SHARED ? 16 : 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -780,7 +779,7 @@ query_x3_kernel(const TcArgs t) {
       }
     }
   } else {
-#if NDF_X3_SHARED_EPI
+    if constexpr (SHARED) {
     // ============ epilogue: all 16 warps serve slot 0 and slot 1 in turn =============
     // Warp (j, wq): TMEM lane quarter wq, columns 64 it + 16 j (it = 0, 1) of every layer,
     // so K-chunk k2 = columns [32 k2, 32 k2 + 32) is finished by warps j = 2 (k2 & 1) + {0, 1}
@@ -889,7 +888,7 @@ query_x3_kernel(const TcArgs t) {
     (void)cnt;
     (void)first;
     (void)d_slot;
-#else
+    } else {
     // ======================== epilogue (slot s, column half ch) ======================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 80;");
     const int ch = wg & 1;
@@ -969,22 +968,24 @@ query_x3_kernel(const TcArgs t) {
           if (l == 0) flush();
         } else {
           if (lead && lane == 0) mbar_arrive(&d_free[s]);
-          float dots[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          if (first_col != 64u * ch) tmem_ld16_nowait(d_base + 64u * ch, va);
-          if (first_col != 64u * ch) tmem_wait_ld();
-#pragma unroll 1
-          for (int kc = 2 * ch; kc < 2 * ch + 2; ++kc) {
-            const int col = 32 * kc;
-            tmem_ld16_nowait(d_base + (uint32_t)(col + 16), vb);
-            dot16_x3<SILU>(va, col, a.m.activation, w32_addr, dots);
-            tmem_wait_ld();
-            if (kc + 1 < 2 * ch + 2) tmem_ld16_nowait(d_base + (uint32_t)(col + 32), va);
-            dot16_x3<SILU>(vb, col + 16, a.m.activation, w32_addr, dots);
-            if (kc + 1 < 2 * ch + 2) tmem_wait_ld();
-          }
+          // the shared epilogue's partials (column groups j = 2 ch, 2 ch + 1: columns 16 j and
+          // 64 + 16 j, in that order) and its summation ((p0 + p1) + (p2 + p3)) + bias, so a
+          // multi-reference cube row equals the single query bit for bit
+          float dA[4] = {0.0f, 0.0f, 0.0f, 0.0f}, dB[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          const uint32_t cA = 32u * (uint32_t)ch, cB = cA + 16u;
+          tmem_ld16_nowait(d_base + cA, va);
+          tmem_ld16_nowait(d_base + cB, vb);
+          tmem_wait_ld();
+          dot16_x3<SILU>(va, (int)cA, a.m.activation, w32_addr, dA);
+          dot16_x3<SILU>(vb, (int)cB, a.m.activation, w32_addr, dB);
+          tmem_ld16_nowait(d_base + 64u + cA, va);
+          tmem_ld16_nowait(d_base + 64u + cB, vb);
+          tmem_wait_ld();
           tc_fence_before();
           if (lane == 0) mbar_arrive(&e2_done[s]);          // this warp's TMEM reads are done
-          const float part = (dots[0] + dots[1]) + (dots[2] + dots[3]);
+          dot16_x3<SILU>(va, 64 + (int)cA, a.m.activation, w32_addr, dA);
+          dot16_x3<SILU>(vb, 64 + (int)cB, a.m.activation, w32_addr, dB);
+          const float part = ((dA[0] + dA[1]) + (dA[2] + dA[3])) + ((dB[0] + dB[1]) + (dB[2] + dB[3]));
           float* dx = dotx + ((kk & 1) * kPPSlots + s) * kTileM;
           if (wq == 0 && lane == 0) NDF_X3_TRACE(s, (int)kk, 20 + ch);
           if (ch == 1) {
@@ -1010,7 +1011,7 @@ query_x3_kernel(const TcArgs t) {
     }
     (void)rng;
     (void)n;
-#endif
+    }
   }
   tc_fence_before();
   __syncthreads();
